@@ -1,0 +1,138 @@
+/*
+ * warpmine_b200.h — C-ABI of libwm_b200.so, the B200-native replacement for
+ * the body of the reference's engine entry point
+ *
+ *     warpmine.engine.run(g: CsrGraph, app: Application, *, mode="wc",
+ *                         warps=4, lane_width=32, balance_config=None)
+ *         -> RunResult                 (pkg/src/warpmine/engine.py:781-843)
+ *
+ * Plain pointers and sizes only.  Host pointers are borrowed for the duration
+ * of the call; device memory is owned by the library.  Calls are blocking and
+ * not re-entrant per graph handle.  Status codes map onto the reference's
+ * exception taxonomy (pkg/src/warpmine/errors.py:4-31) in
+ * paper_2212_04551_b200/_native.py:
+ *
+ *   WM_EINVAL      -> ValueError              (engine.py:791-798, :72-80;
+ *                                              apps.py:38-40, :52-54)
+ *   WM_ECAPACITY   -> CapacityError           (engine.py:319-323)
+ *   WM_EINVARIANT  -> InternalInvariantError  (engine.py:258-261, :472-473;
+ *                                              aggregate.py:190-193)
+ *   WM_ECUDA       -> DeviceError (RuntimeError); no reference counterpart.
+ */
+#ifndef WARPMINE_B200_H
+#define WARPMINE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define WM_ABI_VERSION 1
+
+#define WM_OK 0
+#define WM_EINVAL (-1)
+#define WM_ECAPACITY (-2)
+#define WM_EINVARIANT (-3)
+#define WM_ECUDA (-4)
+
+/* Pipeline filter tags (engine.py:227-237); order-insensitive bit set. */
+#define WM_F_LOWER 1u
+#define WM_F_COMPACT 2u
+#define WM_F_CLIQUE 4u
+#define WM_F_CANONICAL 8u
+
+#define WM_AGG_COUNTER 0 /* aggregate_counter, aggregate.py:169-171 */
+#define WM_AGG_PATTERN 1 /* aggregate_pattern, aggregate.py:174-196 */
+
+#define WM_MODE_WC 1  /* warp-centric, load balancing off  (engine.py:18-19) */
+#define WM_MODE_OPT 2 /* warp-centric + on-device balancer (engine.py:20-21) */
+
+#define WM_ORDER_ID 0     /* clique orientation by vertex id (reference order) */
+#define WM_ORDER_DEGREE 1 /* clique orientation by (degree, id) */
+
+/* CsrGraph (graph.py:28-78): rows ascending, symmetric, no self-loops. */
+typedef struct {
+  int64_t n;                /* vertices */
+  int64_t nnz;              /* 2 * undirected edges */
+  const int64_t *offsets;   /* [n + 1] host */
+  const int32_t *neighbors; /* [nnz] host */
+} wm_csr;
+
+/* Application (engine.py:53-80) as built by clique_app / motif_app
+ * (apps.py:43-58). */
+typedef struct {
+  int k;
+  int extend_all;           /* extend(0, len) vs extend(0, 1) */
+  int genedges;             /* maintain induced-edge bitmaps */
+  int aggregator;           /* WM_AGG_* */
+  uint32_t filters;         /* WM_F_* */
+  const uint32_t *dict_table; /* host, [dict_len]; pattern aggregator only */
+  uint64_t dict_len;
+  uint32_t pattern_count;
+} wm_app;
+
+/* Run configuration: mode / balance_config (balance.py:36-60) plus the
+ * B200-only knobs (root range, sharding, orientation, instrumentation). */
+typedef struct {
+  int mode;                 /* WM_MODE_WC | WM_MODE_OPT */
+  double lb_threshold;      /* donate when active/total warps < threshold
+                               (balance.py:63-66); (0, 1] */
+  int lb_poll;              /* DFS steps between idle-warp polls (>= 1) */
+  int64_t root_begin;       /* root range [root_begin, root_end) over vertex */
+  int64_t root_end;         /*   ids; -1,-1 = all (engine.py:187)           */
+  int shard_rank;           /* cyclic shard of the cost-sorted root tasks */
+  int shard_count;          /*   (multi-GPU, one process per GPU); 1 = all */
+  int order;                /* WM_ORDER_* (clique only) */
+  int count_bytes;          /* 1: instrumented pass computing B_alg (SURVEY
+                               8(d)); forces LB off */
+  int warps_per_block;      /* 0 = auto */
+  int blocks_per_sm;        /* 0 = auto (occupancy) */
+  void *stream;             /* cudaStream_t to run on; NULL = library stream */
+} wm_cfg;
+
+/* RunResult (engine.py:747-762) plus device evidence. */
+typedef struct {
+  uint64_t clique_count;        /* counter aggregator */
+  uint64_t leaves;              /* aggregated_total (engine.py:581, :604) */
+  uint64_t alg_bytes;           /* B_alg when count_bytes, else 0 */
+  uint64_t rebalance_count;     /* donation rounds (idle-triggered polls) */
+  uint64_t migrations;          /* prefixes moved between warps */
+  uint64_t peak_ext;            /* peak extension entries held by one warp */
+  uint64_t *pattern_counts;     /* caller-allocated [pattern_count] or NULL */
+  uint64_t tasks;               /* root tasks processed by this shard */
+  uint64_t launches;            /* kernels launched by this call */
+  uint64_t nodes;               /* internal search-tree nodes expanded */
+  uint64_t polls;               /* idle-counter polls by busy warps (opt) */
+  double kernel_ms;             /* enumeration kernel(s), CUDA events */
+  double device_ms;             /* whole call on the device incl. preprocessing */
+  double idle_warp_fraction;    /* idle warp-time / (warps * kernel time) */
+  double idle_warp_fraction_tail; /* same, from the first root-queue drain */
+  int warps;                    /* resident warps of the enumeration kernel */
+  int bucket_words;             /* clique bitmap words per row (max bucket) */
+} wm_result;
+
+/* Upload a CSR graph to the current device (cudaSetDevice beforehand). */
+int wm_graph_create(const wm_csr *csr, void **graph);
+
+/* Same, from device-resident arrays (copied device-to-device). */
+int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
+                           const int32_t *d_neighbors, void **graph);
+
+/* engine.run: enumerate every canonical size-k traversal rooted in the
+ * configured root set.  Fills *result; pattern_counts must hold
+ * app->pattern_count entries for the pattern aggregator. */
+int wm_run(void *graph, const wm_app *app, const wm_cfg *cfg, wm_result *result);
+
+void wm_graph_destroy(void *graph);
+
+/* Message of the last failing call on this thread ("" if none). */
+const char *wm_last_error(void);
+
+int wm_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WARPMINE_B200_H */

@@ -1,0 +1,252 @@
+// wm_api.cu — the C-ABI entry points of libwm_b200.so (include/warpmine_b200.h).
+//
+// wm_run replaces the body of warpmine.engine.run (reference
+// pkg/src/warpmine/engine.py:781-843): argument checks mirror :791-798 and
+// Application validation :72-80; dispatch picks the clique kernel for the
+// clique_app pipeline (apps.py:43-47) and the motif kernel for motif_app
+// (apps.py:50-58).  Any other pipeline is rejected with WM_EINVAL — there is
+// no CPU fallback.
+#include <cstdarg>
+#include <cstring>
+#include <string>
+
+#include "wm_common.cuh"
+
+namespace wm {
+
+static thread_local std::string g_last_error;
+
+void set_error(const std::string &msg) { g_last_error = msg; }
+
+int fail(int code, const char *fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int DeviceBuffer::ensure(size_t want) {
+  if (want <= bytes && ptr) return WM_OK;
+  release();
+  size_t b = want < 256 ? 256 : want;
+  cudaError_t e = cudaMalloc(&ptr, b);
+  if (e != cudaSuccess) {
+    ptr = nullptr;
+    bytes = 0;
+    return fail(WM_ECUDA, "cudaMalloc(%zu) failed: %s", b, cudaGetErrorString(e));
+  }
+  bytes = b;
+  return WM_OK;
+}
+
+void DeviceBuffer::release() {
+  if (ptr) cudaFree(ptr);
+  ptr = nullptr;
+  bytes = 0;
+}
+
+__global__ void lb_init_kernel(LbState *lb, int total_warps, uint32_t *ring, uint32_t cap) {
+  const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+  if (tid == 0) {
+    LbState z;
+    memset(&z, 0, sizeof z);
+    z.active = total_warps;
+    z.total_warps = total_warps;
+    z.t_start_min = ~0ull;
+    z.t_tail_min = ~0ull;
+    z.t_base = globaltimer_ns();
+    *lb = z;
+  }
+  if (ring)
+    for (uint32_t i = tid; i < cap; i += gridDim.x * blockDim.x) ring[(size_t)i * kSlotWords] = 0u;
+}
+
+int lb_prepare(Graph *g, LbState *lb, int warps, uint32_t words, LbShared *out, cudaStream_t s) {
+  uint32_t cap = 1;
+  while (cap < 8u * (uint32_t)warps) cap <<= 1;
+  int st;
+  if ((st = g->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap))) return st;
+  out->lb = lb;
+  out->ring = g->ring.as<uint32_t>();
+  out->cap = cap;
+  out->words = words;
+  lb_init_kernel<<<(int)((cap + 255) / 256), 256, 0, s>>>(lb, warps, out->ring, cap);
+  WM_CUDA(cudaGetLastError());
+  return WM_OK;
+}
+
+void finish_lb_stats(const LbState &h, wm_result *res) {
+  const double W = (double)h.total_warps;
+  const double T0 = (double)h.t_start_min, T1 = (double)h.t_end_max;
+  if (W <= 0 || T1 <= T0) {
+    res->idle_warp_fraction = 0;
+    res->idle_warp_fraction_tail = 0;
+    return;
+  }
+  // idle = waiting in acquire_work + after exit + before first start
+  const double after_exit = W * T1 - (double)h.sum_end;
+  const double before_start = (double)h.sum_start - W * T0;
+  const double idle = (double)h.sum_idle_ns + after_exit + before_start;
+  res->idle_warp_fraction = idle / (W * (T1 - T0));
+  double Tt = (double)h.t_tail_min;
+  if (Tt < T0 || Tt > T1 || h.t_tail_min == ~0ull) Tt = T1;
+  res->idle_warp_fraction_tail =
+      (T1 > Tt) ? ((double)h.sum_tail_idle_ns + after_exit) / (W * (T1 - Tt)) : 0.0;
+  if (res->idle_warp_fraction_tail > 1.0) res->idle_warp_fraction_tail = 1.0;
+  res->migrations = h.migrations;
+  res->rebalance_count = h.donation_polls;
+  res->peak_ext = h.peak_ext;
+}
+
+}  // namespace wm
+
+using namespace wm;
+
+extern "C" {
+
+int wm_abi_version(void) { return WM_ABI_VERSION; }
+
+const char *wm_last_error(void) { return g_last_error.c_str(); }
+
+static int graph_init(Graph *g) {
+  WM_CUDA(cudaGetDevice(&g->device));
+  WM_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
+  WM_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+  return WM_OK;
+}
+
+int wm_graph_create(const wm_csr *csr, void **out) {
+  g_last_error.clear();
+  if (!csr || !out) return fail(WM_EINVAL, "null argument");
+  if (csr->n < 1) return fail(WM_EINVAL, "graph needs at least one vertex, got n=%lld",
+                              (long long)csr->n);
+  if (csr->n >= (1ll << 31) - 1) return fail(WM_EINVAL, "n=%lld exceeds int32 vertex ids",
+                                             (long long)csr->n);
+  if (!csr->offsets || (csr->nnz > 0 && !csr->neighbors))
+    return fail(WM_EINVAL, "null CSR arrays");
+  if (csr->offsets[0] != 0 || csr->offsets[csr->n] != csr->nnz)
+    return fail(WM_EINVAL, "offsets do not span nnz=%lld", (long long)csr->nnz);
+  Graph *g = new Graph();
+  int st = graph_init(g);
+  if (st) { delete g; return st; }
+  g->n = csr->n;
+  g->nnz = csr->nnz;
+  int64_t md = 0;
+  for (int64_t v = 0; v < csr->n; ++v) {
+    int64_t d = csr->offsets[v + 1] - csr->offsets[v];
+    if (d < 0) { delete g; return fail(WM_EINVAL, "offsets decrease at vertex %lld", (long long)v); }
+    if (d > md) md = d;
+  }
+  g->max_degree = md;
+  cudaError_t e = cudaMalloc(&g->offsets, sizeof(int64_t) * (g->n + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&g->neighbors, sizeof(int32_t) * (g->nnz > 0 ? g->nnz : 1));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(g->offsets, csr->offsets, sizeof(int64_t) * (g->n + 1),
+                        cudaMemcpyHostToDevice, g->own_stream);
+  if (e == cudaSuccess && g->nnz > 0)
+    e = cudaMemcpyAsync(g->neighbors, csr->neighbors, sizeof(int32_t) * g->nnz,
+                        cudaMemcpyHostToDevice, g->own_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->own_stream);
+  if (e != cudaSuccess) {
+    wm_graph_destroy(g);
+    return fail(WM_ECUDA, "graph upload failed: %s", cudaGetErrorString(e));
+  }
+  *out = g;
+  return WM_OK;
+}
+
+int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
+                           const int32_t *d_neighbors, void **out) {
+  g_last_error.clear();
+  if (!out || !d_offsets || n < 1) return fail(WM_EINVAL, "bad device graph arguments");
+  Graph *g = new Graph();
+  int st = graph_init(g);
+  if (st) { delete g; return st; }
+  g->n = n;
+  g->nnz = nnz;
+  cudaError_t e = cudaMalloc(&g->offsets, sizeof(int64_t) * (n + 1));
+  if (e == cudaSuccess) e = cudaMalloc(&g->neighbors, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(g->offsets, d_offsets, sizeof(int64_t) * (n + 1),
+                        cudaMemcpyDeviceToDevice, g->own_stream);
+  if (e == cudaSuccess && nnz > 0)
+    e = cudaMemcpyAsync(g->neighbors, d_neighbors, sizeof(int32_t) * nnz,
+                        cudaMemcpyDeviceToDevice, g->own_stream);
+  // max degree for capacity planning
+  int64_t *h_off = nullptr;
+  if (e == cudaSuccess) e = cudaMallocHost(&h_off, sizeof(int64_t) * (n + 1));
+  if (e == cudaSuccess)
+    e = cudaMemcpyAsync(h_off, d_offsets, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost,
+                        g->own_stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(g->own_stream);
+  if (e == cudaSuccess) {
+    for (int64_t v = 0; v < n; ++v)
+      if (h_off[v + 1] - h_off[v] > g->max_degree) g->max_degree = h_off[v + 1] - h_off[v];
+  }
+  if (h_off) cudaFreeHost(h_off);
+  if (e != cudaSuccess) {
+    wm_graph_destroy(g);
+    return fail(WM_ECUDA, "device graph copy failed: %s", cudaGetErrorString(e));
+  }
+  *out = g;
+  return WM_OK;
+}
+
+void wm_graph_destroy(void *gp) {
+  Graph *g = static_cast<Graph *>(gp);
+  if (!g) return;
+  if (g->offsets) cudaFree(g->offsets);
+  if (g->neighbors) cudaFree(g->neighbors);
+  if (g->own_stream) cudaStreamDestroy(g->own_stream);
+  delete g;
+}
+
+int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
+  g_last_error.clear();
+  Graph *g = static_cast<Graph *>(gp);
+  if (!g || !app || !cfg || !res) return fail(WM_EINVAL, "null argument");
+  // engine.py:791-798 / balance.py:48-52
+  if (cfg->mode != WM_MODE_WC && cfg->mode != WM_MODE_OPT)
+    return fail(WM_EINVAL, "mode must be wc or opt (dfs has no device path)");
+  if (cfg->mode == WM_MODE_OPT && !(cfg->lb_threshold > 0.0 && cfg->lb_threshold <= 1.0))
+    return fail(WM_EINVAL, "threshold must be in (0, 1]");
+  if (cfg->mode == WM_MODE_OPT && cfg->lb_poll < 1)
+    return fail(WM_EINVAL, "poll_interval must be >= 1");
+  if (cfg->shard_count < 1 || cfg->shard_rank < 0 || cfg->shard_rank >= cfg->shard_count)
+    return fail(WM_EINVAL, "bad shard %d/%d", cfg->shard_rank, cfg->shard_count);
+  // engine.py:72-80, apps.py:38-58
+  if (app->k < 3) return fail(WM_EINVAL, "need k >= 3");
+  const bool clique = app->aggregator == WM_AGG_COUNTER && !app->extend_all &&
+                      (app->filters & WM_F_CLIQUE) && (app->filters & WM_F_LOWER) &&
+                      !(app->filters & WM_F_CANONICAL);
+  const bool motif = app->aggregator == WM_AGG_PATTERN && app->extend_all && app->genedges &&
+                     app->filters == WM_F_CANONICAL;
+  uint64_t *user_hist = res->pattern_counts;
+  memset(res, 0, sizeof *res);
+  res->pattern_counts = user_hist;
+  cudaStream_t s = cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : g->own_stream;
+  int dev = 0;
+  WM_CUDA(cudaGetDevice(&dev));
+  if (dev != g->device)
+    return fail(WM_EINVAL, "graph lives on device %d, current device is %d", g->device, dev);
+  if (clique) {
+    if (app->k > 12) return fail(WM_EINVAL, "k must be in [3, 12], got %d", app->k);
+    return run_clique(g, app, cfg, res, s);
+  }
+  if (motif) {
+    if (app->k > 8) return fail(WM_EINVAL, "k must be in [3, 8], got %d", app->k);
+    if (!app->dict_table || app->dict_len != (1ull << (app->k * (app->k - 1) / 2 - 1)) ||
+        app->pattern_count < 1)
+      return fail(WM_EINVAL, "pattern aggregation requires the k=%d dictionary", app->k);
+    if (!user_hist) return fail(WM_EINVAL, "pattern_counts buffer required");
+    return run_motif(g, app, cfg, res, s);
+  }
+  return fail(WM_EINVAL,
+              "pipeline not supported on the device: only the built-in clique_app and "
+              "motif_app pipelines run (no CPU fallback)");
+}
+
+}  // extern "C"

@@ -1,0 +1,739 @@
+// wm_clique.cu — warp-centric k-clique counting (clique_app, reference
+// pkg/src/warpmine/apps.py:43-47) for sm_100a.
+//
+// Reference pipeline per traversal (engine.py:214-241):
+//   extend(0,1)      N(tr[0]) minus tr                    engine.py:245-327
+//   filter_lower     drop e <= tr[len-1]                  engine.py:331-353
+//   compact          stable removal of invalid entries    engine.py:544-564
+//   filter_clique    keep e adjacent to every tr[j]       engine.py:355-422
+//   aggregate        count_valid at len == k-1            engine.py:568-592,
+//                                                         aggregate.py:155-171
+//   move_step        pop one pending extension, descend   engine.py:643-676
+//
+// B200 restatement.  The clique tree's level-L extension set is
+//   C_L = { e in N(tr[0]) : e above tr[L-1], e adjacent to tr[0..L) }
+// which, since the filters are conjunctive, equals C_{L-1} ∩ N+(tr[L-1])
+// with N+ the out-neighbours of an orientation ("lower" = above in the
+// order).  Per root task the warp stages N+(root) in shared memory and builds
+// the induced DAG among those d vertices as a d x d bitmap (sorted-set
+// intersections of N+(u_i) against N+(root), binary search in smem).  Every
+// later extension is then one W-word AND (extend + lower + clique fused),
+// compaction is implicit in the bitmap, and the last two levels are
+// aggregated in bulk: sum over j in C of popc(C & A[j]) — each lane takes one
+// member j (ballot-free: lane l owns bit l of every word).  Counts are
+// orientation-invariant; WM_ORDER_ID reproduces the
+// reference's id order exactly, WM_ORDER_DEGREE bounds d by the degeneracy.
+//
+// Work distribution: persistent warps pull root tasks (cost-sorted, largest
+// first) from a global cursor (the engine's root deque, engine.py:187).  In
+// opt mode busy warps poll the idle-warp counter and donate their shallowest
+// pending extension (balance.py:102-155 semantics: the thief owns exactly the
+// stolen branch; inherited levels are never regenerated).
+#include <cub/cub.cuh>
+
+#include "wm_common.cuh"
+
+namespace wm {
+
+// --------------------------------------------------------------------------
+// orientation: u is "above" v
+
+__device__ __forceinline__ bool above(int order, int64_t du, int32_t u, int64_t dv, int32_t v) {
+  if (order == WM_ORDER_ID) return u > v;
+  return du > dv || (du == dv && u > v);
+}
+
+__global__ void orient_count_kernel(int64_t n, const int64_t *__restrict__ off,
+                                    const int32_t *__restrict__ nbr, int order,
+                                    int32_t *__restrict__ outdeg) {
+  const int lane = lane_id();
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = off[v], e = off[v + 1], dv = e - b;
+    int cnt = 0;
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int32_t u = __ldg(nbr + p);
+      const int64_t du = order == WM_ORDER_ID ? 0 : __ldg(off + u + 1) - __ldg(off + u);
+      cnt += above(order, du, u, dv, (int32_t)v);
+    }
+    cnt = __reduce_add_sync(0xffffffffu, cnt);
+    if (lane == 0) outdeg[v] = cnt;
+  }
+}
+
+// ballot+popc stream compaction of the "above" neighbours, order preserved
+__global__ void orient_fill_kernel(int64_t n, const int64_t *__restrict__ off,
+                                   const int32_t *__restrict__ nbr, int order,
+                                   const int64_t *__restrict__ doff, int32_t *__restrict__ dnbr) {
+  const int lane = lane_id();
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = off[v], e = off[v + 1], dv = e - b;
+    int64_t w = doff[v];
+    for (int64_t p0 = b; p0 < e; p0 += 32) {
+      const int64_t p = p0 + lane;
+      bool keep = false;
+      int32_t u = 0;
+      if (p < e) {
+        u = __ldg(nbr + p);
+        const int64_t du = order == WM_ORDER_ID ? 0 : __ldg(off + u + 1) - __ldg(off + u);
+        keep = above(order, du, u, dv, (int32_t)v);
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) dnbr[w + __popc(bal & ((1u << lane) - 1))] = u;
+      w += __popc(bal);
+    }
+  }
+}
+
+// sort keys: eligible roots (out-degree >= k-1, inside the root range) get
+// outdeg+1, others 0; values are vertex ids in ascending order so the stable
+// descending sort is deterministic (identical task lists on every rank).
+__global__ void task_keys_kernel(int64_t n, const int32_t *__restrict__ outdeg, int k,
+                                 int64_t rb, int64_t re, uint32_t *__restrict__ keys,
+                                 int32_t *__restrict__ vals) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const bool ok = v >= rb && v < re && outdeg[v] >= k - 1;
+    keys[v] = ok ? (uint32_t)outdeg[v] + 1u : 0u;
+    vals[v] = (int32_t)v;
+  }
+}
+
+// counts[c] = number of eligible tasks whose bitmap needs 2^c words per row
+// (c = 0..5 -> W = 1..32, d <= 32W); counts[6] = over-capacity (d > 1024).
+__global__ void bucket_count_kernel(int64_t n, const uint32_t *__restrict__ keys,
+                                    unsigned long long *__restrict__ counts) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t key = keys[i];
+    if (!key) continue;
+    const uint32_t d = key - 1;
+    int c = 0;
+    while (c < 6 && d > (32u << c)) ++c;
+    atomicAdd(&counts[c], 1ull);
+  }
+}
+
+// words of the compact local bitmap of a root with out-degree d
+__device__ __host__ __forceinline__ unsigned long long bm_words(int d) {
+  return (unsigned long long)d * (unsigned long long)((d + 31) >> 5);
+}
+
+__global__ void task_words_kernel(unsigned long long ntask, const uint32_t *__restrict__ keys,
+                                  unsigned long long *__restrict__ words) {
+  for (unsigned long long t = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+       t < ntask; t += (unsigned long long)gridDim.x * blockDim.x)
+    words[t] = bm_words((int)keys[t] - 1);
+}
+
+// --------------------------------------------------------------------------
+// 1) per-root local DAG bitmaps, built once into an HBM arena
+//
+// Root task t (vertex v, d = |N+(v)|) owns rows [bm_off[t], bm_off[t] + d*Wv)
+// with Wv = ceil(d/32): row i = N+(u_i) ∩ N+(v) as local bit positions, u_i
+// the i-th out-neighbour of v in ascending id.  These rows are the reference's
+// filter_clique + filter_lower predicates (engine.py:331-422) precomputed for
+// every pair inside the root's extension set, so every later extension is a
+// W-word AND.  Total size is sum_v d_v * ceil(d_v/32) words (2.6 MB at cfg3).
+
+template <int W> struct BuildSmem {
+  static constexpr int D = 32 * W;
+  int32_t list[D];
+  uint32_t adj[D * W];
+  int32_t pre[D + 1];
+  int64_t rowbeg[D];
+};
+
+template <int W>
+__global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__restrict__ doff,
+                                                           const int32_t *__restrict__ dnbr,
+                                                           const int32_t *__restrict__ tasks,
+                                                           unsigned long long ntask,
+                                                           const unsigned long long *__restrict__ bm_off,
+                                                           uint32_t *__restrict__ bm) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  BuildSmem<W> &sm = reinterpret_cast<BuildSmem<W> *>(smraw)[threadIdx.x >> 5];
+  const int lane = lane_id();
+  const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  for (unsigned long long t = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+       t < ntask; t += nwarps) {
+    const int32_t v = __ldg(tasks + t);
+    const int64_t b = __ldg(doff + v);
+    const int d = (int)(__ldg(doff + v + 1) - b);
+    const int wv = (d + 31) >> 5;
+    for (int i = lane; i < d; i += 32) {
+      const int32_t u = __ldg(dnbr + b + i);
+      const int64_t rb = __ldg(doff + u), re = __ldg(doff + u + 1);
+      sm.list[i] = u;
+      sm.rowbeg[i] = rb;
+      sm.pre[i] = (int)(re - rb);
+    }
+    for (int i = lane; i < d * wv; i += 32) sm.adj[i] = 0u;
+    __syncwarp();
+    int carry = 0;
+    for (int base = 0; base < d; base += 32) {
+      const int i = base + lane;
+      const int x = i < d ? sm.pre[i] : 0;
+      int y = x;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int z = __shfl_up_sync(0xffffffffu, y, o);
+        if (lane >= o) y += z;
+      }
+      if (i < d) sm.pre[i] = carry + y - x;
+      carry += __shfl_sync(0xffffffffu, y, 31);
+    }
+    __syncwarp();
+    const int total = carry;
+    // flattened (row, element) pairs: every lane busy regardless of row length
+    for (int f0 = 0; f0 < total; f0 += 128) {
+      int32_t xs[4];
+      int rows[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int f = f0 + j * 32 + lane;
+        rows[j] = -1;
+        if (f < total) {
+          int lo = 0, hi = d;  // last row with pre <= f
+          while (hi - lo > 1) {
+            const int mid = (lo + hi) >> 1;
+            if (sm.pre[mid] <= f) lo = mid; else hi = mid;
+          }
+          rows[j] = lo;
+          xs[j] = __ldg(dnbr + sm.rowbeg[lo] + (f - sm.pre[lo]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (rows[j] >= 0) {
+          const int pos = lower_bound_i(sm.list, d, xs[j]);
+          if (pos < d && sm.list[pos] == xs[j])
+            atomicOr(&sm.adj[rows[j] * wv + (pos >> 5)], 1u << (pos & 31));
+        }
+      }
+    }
+    __syncwarp();
+    uint32_t *out = bm + bm_off[t];
+    for (int i = lane; i < d * wv; i += 32) out[i] = sm.adj[i];
+    __syncwarp();
+  }
+}
+
+// --------------------------------------------------------------------------
+// 2) enumeration: per-warp DFS-wide stack in shared memory
+
+template <int W> struct CliqueSmem {
+  static constexpr int D = 32 * W;                // max local vertices
+  static constexpr int S = (W == 1) ? 1 : W + 1;  // odd row stride: conflict-free bulk reads
+  uint32_t adj[D * S];                            // local DAG rows of the current root
+  uint32_t C[kMaxK][W];                           // candidate set per level
+  uint32_t P[kMaxK][W];                           // unconsumed members per level
+  unsigned long long below[kMaxK];                // leaves under the level's node (B_alg)
+  int32_t last[kMaxK];                            // vertex appended at the level
+};
+
+struct CliqueArgs {
+  const int64_t *doff;
+  const int32_t *dnbr;
+  const int32_t *tasks;           // bucket's cost-sorted roots
+  const unsigned long long *bm_off;  // bucket's bitmap offsets (per task)
+  const uint32_t *bm;             // bitmap arena
+  unsigned long long ntasks;      // tasks of this shard in the bucket
+  unsigned long long task_offset; // shard rank
+  unsigned long long task_stride; // shard count
+  int k;
+  int lb_on;
+  int lb_poll;
+  int idle_min;
+  LbShared L;
+  unsigned long long *counters;   // [0] cliques [1] B_alg [2] tasks [3] nodes [4] polls
+};
+
+// Leaves under a node at traversal length k-2 with candidate set C[s]:
+// for each member j (lane l owns bit l of each word) popc(C & A[j]).
+// Returns this lane's partial; with BYTES also adds B_alg of the length-(k-1)
+// nodes and returns the warp total in `warp_total`.
+template <int W, bool BYTES>
+__device__ __forceinline__ unsigned long long bulk_count(const CliqueSmem<W> &sm, int s,
+                                                         const CliqueArgs &a, int64_t list_base,
+                                                         unsigned long long &bytes,
+                                                         unsigned long long &warp_total) {
+  constexpr int S = CliqueSmem<W>::S;
+  const int lane = lane_id();
+  uint32_t c[W];
+#pragma unroll
+  for (int x = 0; x < W; ++x) c[x] = sm.C[s][x];
+  unsigned long long part = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    if (c[w] == 0u) continue;
+    if ((c[w] >> lane) & 1u) {
+      const int j = w * 32 + lane;
+      const uint32_t *row = sm.adj + j * S;
+      uint32_t t = 0;
+#pragma unroll
+      for (int x = 0; x < W; ++x) t += __popc(c[x] & row[x]);
+      part += t;
+      if (BYTES && t) {
+        const int32_t u = __ldg(a.dnbr + list_base + j);
+        bytes += 4ull * (unsigned long long)(__ldg(a.doff + u + 1) - __ldg(a.doff + u));
+      }
+    }
+  }
+  if (BYTES) warp_total = warp_sum_u64(part);
+  return part;
+}
+
+// Donate the upper half of the pending members of the shallowest level that
+// has any (reference balance.py:102-128 steals the shallowest pending entry;
+// one record here carries half of that level so a thief gets a large
+// subtree).  Record: [task, level, C[level] (W words), donated P (W words)].
+// Subtrees estimated below ~4K nodes are not worth a move and stay.
+constexpr int kRecHdr = 2;
+
+template <int W>
+__device__ __forceinline__ void try_donate(CliqueSmem<W> &sm, const CliqueArgs &a, int s0, int s,
+                                           unsigned long long task) {
+  const int lane = lane_id();
+  int sd = -1;
+  uint32_t pw = 0u;
+  for (int t = s0; t <= s; ++t) {
+    const uint32_t w2 = lane < W ? sm.P[t][lane] : 0u;
+    if (__ballot_sync(0xffffffffu, w2 != 0u)) { sd = t; pw = w2; break; }
+  }
+  if (sd < 0) return;
+  const uint32_t cw = lane < W ? sm.C[sd][lane] : 0u;
+  const int cnt = __popc(pw);
+  int pre = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int z = __shfl_up_sync(0xffffffffu, pre, o);
+    if (lane >= o) pre += z;
+  }
+  const int total = __shfl_sync(0xffffffffu, pre, 31);
+  const int csize = __reduce_add_sync(0xffffffffu, __popc(cw));
+  const int depth = a.k - 2 - sd;  // DFS levels below, bulk level included
+  const float est = (float)total * __powf((float)csize, (float)(depth - 1));
+  if (est < 4096.f) return;
+  pre -= cnt;  // exclusive prefix
+  const int keep = total / 2;
+  uint32_t give;
+  if (pre >= keep) give = pw;
+  else if (pre + cnt <= keep) give = 0u;
+  else {
+    uint32_t w2 = pw;
+    for (int r = keep - pre; r > 0; --r) w2 &= w2 - 1u;
+    give = w2;
+  }
+  Rec3 rec;
+#pragma unroll
+  for (int r = 0; r < 3; ++r) {
+    const int idx = 32 * r + lane;
+    const uint32_t cv = __shfl_sync(0xffffffffu, cw, (idx - kRecHdr) & 31);
+    const uint32_t gv = __shfl_sync(0xffffffffu, give, (idx - kRecHdr - W) & 31);
+    rec.w[r] = idx == 0 ? (uint32_t)task
+             : idx == 1 ? (uint32_t)sd
+             : (idx - kRecHdr < W ? cv : (idx - kRecHdr - W < W ? gv : 0u));
+  }
+  donate_record(a.L, rec);
+  if (lane < W) sm.P[sd][lane] = pw & ~give;
+  const int moved = __reduce_add_sync(0xffffffffu, __popc(give));
+  if (lane == 0) {
+    atomicAdd(&a.L.lb->migrations, (unsigned long long)moved);
+    atomicAdd(&a.L.lb->donation_polls, 1ull);
+  }
+  __syncwarp();
+}
+
+template <int W, bool BYTES>
+__global__ void __launch_bounds__(256) clique_enum_kernel(CliqueArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  CliqueSmem<W> &sm = reinterpret_cast<CliqueSmem<W> *>(smraw)[threadIdx.x >> 5];
+  constexpr int S = CliqueSmem<W>::S;
+  const int lane = lane_id();
+  const int k = a.k;
+  WarpClock clk;
+  warp_clock_begin(clk, a.L.lb);
+  bool roots_left = true;
+  unsigned long long acc = 0, bytes = 0, tasks_done = 0, nodes = 0, polls = 0;
+  int poll = 0;
+  unsigned long long cached = ~0ull;
+  for (;;) {
+    unsigned long long ti = 0;
+    Rec3 rec = {{0u, 0u, 0u}};
+    const int kind = acquire_work(a.L, a.lb_on, a.ntasks, roots_left, ti, rec, clk);
+    if (kind == 0) break;
+    unsigned long long task;
+    int s0;
+    if (kind == 1) {
+      task = a.task_offset + ti * a.task_stride;
+      s0 = 1;
+    } else {
+      task = __shfl_sync(0xffffffffu, rec.w[0], 0);
+      s0 = (int)__shfl_sync(0xffffffffu, rec.w[0], 1);
+    }
+    const int32_t root = __ldg(a.tasks + task);
+    const int64_t list_base = __ldg(a.doff + root);
+    const int d = (int)(__ldg(a.doff + root + 1) - list_base);
+    if (task != cached) {
+      // stage the root's rows from the arena (L2-resident) into smem
+      const int wv = (d + 31) >> 5;
+      const uint32_t *src = a.bm + __ldg(a.bm_off + task);
+      for (int i = lane; i < d * wv; i += 32) {
+        const int r = i / wv, x = i - r * wv;
+        sm.adj[r * S + x] = __ldg(src + i);
+      }
+      cached = task;
+    }
+    {
+      // donated record: words 2..W+1 = C[s0], W+2..2W+1 = pending subset
+      const uint32_t cv = rec_word(rec, kRecHdr + lane);
+      const uint32_t pv = rec_word(rec, kRecHdr + W + lane);
+      if (lane < W) {
+        uint32_t cword, pword;
+        if (kind == 1) {
+          const int lo = lane * 32;
+          cword = d >= lo + 32 ? 0xffffffffu : (d > lo ? (1u << (d - lo)) - 1u : 0u);
+          pword = cword;
+        } else {
+          cword = cv;
+          pword = pv;
+        }
+        sm.C[s0][lane] = cword;
+        sm.P[s0][lane] = pword;
+      }
+    }
+    if (lane == 0) {
+      sm.below[s0] = 0;
+      sm.last[s0] = root;
+    }
+    __syncwarp();
+    tasks_done += (kind == 1);
+    if (s0 == k - 2) {
+      unsigned long long tot = 0;
+      acc += bulk_count<W, BYTES>(sm, s0, a, list_base, bytes, tot);
+      if (BYTES && lane == 0 && tot)
+        bytes += 4ull * (unsigned long long)(__ldg(a.doff + root + 1) - __ldg(a.doff + root));
+      continue;
+    }
+    int s = s0;
+    for (;;) {
+      // move_step: next unconsumed member at level s (lowest set bit)
+      const uint32_t pw = lane < W ? sm.P[s][lane] : 0u;
+      const unsigned nz = __ballot_sync(0xffffffffu, pw != 0u);
+      if (nz == 0u) {
+        if (BYTES && lane == 0) {
+          const unsigned long long b = sm.below[s];
+          if (b) {
+            const int32_t x = sm.last[s];
+            bytes += 4ull * (unsigned long long)(__ldg(a.doff + x + 1) - __ldg(a.doff + x));
+            if (s > s0) sm.below[s - 1] += b;
+          }
+        }
+        __syncwarp();
+        if (s == s0) break;
+        --s;
+        continue;
+      }
+      const int wl = __ffs(nz) - 1;
+      const uint32_t word = __shfl_sync(0xffffffffu, pw, wl);
+      const int i = wl * 32 + __ffs(word) - 1;
+      if (lane == wl) sm.P[s][wl] = word & (word - 1u);
+      // extend + lower + clique, fused: C_{s+1} = C_s & A[i]
+      uint32_t cw = 0u;
+      if (lane < W) {
+        cw = sm.C[s][lane] & sm.adj[i * S + lane];
+        sm.C[s + 1][lane] = cw;
+      }
+      const int cnt = __reduce_add_sync(0xffffffffu, __popc(cw));
+      __syncwarp();
+      ++nodes;
+      if (cnt >= k - s - 1) {
+        if (s + 1 == k - 2) {
+          unsigned long long tot = 0;
+          acc += bulk_count<W, BYTES>(sm, s + 1, a, list_base, bytes, tot);
+          if (BYTES && lane == 0 && tot) {
+            const int32_t x = __ldg(a.dnbr + list_base + i);
+            bytes += 4ull * (unsigned long long)(__ldg(a.doff + x + 1) - __ldg(a.doff + x));
+            sm.below[s] += tot;
+          }
+          __syncwarp();
+        } else {
+          ++s;
+          if (lane < W) sm.P[s][lane] = cw;
+          if (BYTES && lane == 0) {
+            sm.below[s] = 0;
+            sm.last[s] = __ldg(a.dnbr + list_base + i);
+          }
+          __syncwarp();
+        }
+      }
+      // on-device load balancing (opt mode): poll the idle-warp ring
+      if (!BYTES && a.lb_on && ++poll >= a.lb_poll) {
+        poll = 0;
+        ++polls;
+        if (donation_wanted(a.L, a.idle_min)) try_donate<W>(sm, a, s0, s, task);
+      }
+    }
+  }
+  acc = warp_sum_u64(acc);
+  if (BYTES) bytes = warp_sum_u64(bytes);
+  if (lane == 0) {
+    atomicAdd(&a.counters[0], acc);
+    if (BYTES) atomicAdd(&a.counters[1], bytes);
+    atomicAdd(&a.counters[2], tasks_done);
+    atomicAdd(&a.counters[3], nodes);
+    atomicAdd(&a.counters[4], polls);
+  }
+  warp_clock_end(a.L.lb, clk);
+}
+
+// --------------------------------------------------------------------------
+// host launcher
+
+template <int W>
+static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask, cudaStream_t s) {
+  const size_t per_warp = sizeof(BuildSmem<W>);
+  int wpb = 8;
+  while (wpb > 1 && per_warp * wpb > 200 * 1024) wpb >>= 1;
+  const size_t smem = per_warp * wpb;
+  auto kern = clique_build_kernel<W>;
+  WM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int bps = 0;
+  WM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
+  if (bps < 1) return fail(WM_ECAPACITY, "clique build kernel W=%d does not fit on an SM", W);
+  unsigned long long blocks = (unsigned long long)g->num_sms * bps;
+  const unsigned long long need = (ntask + wpb - 1) / wpb;
+  if (blocks > need) blocks = need;
+  kern<<<(int)blocks, wpb * 32, smem, s>>>(a.doff, a.dnbr, a.tasks, ntask, a.bm_off,
+                                           const_cast<uint32_t *>(a.bm));
+  WM_CUDA(cudaGetLastError());
+  return WM_OK;
+}
+
+template <int W, bool BYTES>
+static int launch_enum(Graph *g, const wm_cfg *cfg, CliqueArgs a, cudaStream_t s,
+                       int *warps_out) {
+  const size_t per_warp = sizeof(CliqueSmem<W>);
+  int wpb = cfg->warps_per_block > 0 ? cfg->warps_per_block : 8;
+  while (wpb > 1 && per_warp * wpb > 200 * 1024) wpb >>= 1;
+  const size_t smem = per_warp * wpb;
+  auto kern = clique_enum_kernel<W, BYTES>;
+  WM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  int bps = 0;
+  WM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
+  if (cfg->blocks_per_sm > 0 && cfg->blocks_per_sm < bps) bps = cfg->blocks_per_sm;
+  if (bps < 1) return fail(WM_ECAPACITY, "clique kernel W=%d does not fit on an SM", W);
+  int blocks = g->num_sms * bps;
+  if (!a.lb_on) {  // no stealing: no point in more warps than tasks
+    const unsigned long long need = (a.ntasks + wpb - 1) / wpb;
+    if ((unsigned long long)blocks > need) blocks = (int)(need > 0 ? need : 1);
+  }
+  const int warps = blocks * wpb;
+  int st = lb_prepare(g, a.L.lb, warps, (uint32_t)(kRecHdr + 2 * W), &a.L, s);
+  if (st) return st;
+  a.idle_min = (int)((1.0 - cfg->lb_threshold) * warps);
+  if (a.idle_min < 1) a.idle_min = 1;
+  kern<<<blocks, wpb * 32, smem, s>>>(a);
+  WM_CUDA(cudaGetLastError());
+  *warps_out = warps;
+  return WM_OK;
+}
+
+int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s) {
+  const int64_t n = g->n;
+  const int k = app->k;
+  const int order = cfg->order == WM_ORDER_ID ? WM_ORDER_ID : WM_ORDER_DEGREE;
+  const bool bytes = cfg->count_bytes != 0;
+  const bool lb_on = cfg->mode == WM_MODE_OPT && !bytes;
+  int st;
+  if ((st = g->dag_off.ensure(sizeof(int64_t) * (n + 1)))) return st;
+  if ((st = g->outdeg.ensure(sizeof(int32_t) * (n + 1)))) return st;
+  if ((st = g->dag_nbr.ensure(sizeof(int32_t) * (g->nnz / 2 + 1)))) return st;
+  if ((st = g->keys_in.ensure(sizeof(uint32_t) * n))) return st;
+  if ((st = g->keys_out.ensure(sizeof(uint32_t) * n))) return st;
+  if ((st = g->vals_in.ensure(sizeof(int32_t) * n))) return st;
+  if ((st = g->vals_out.ensure(sizeof(int32_t) * n))) return st;
+  if ((st = g->hist.ensure(sizeof(unsigned long long) * (n + 1)))) return st;  // task words
+  if ((st = g->table.ensure(sizeof(unsigned long long) * (n + 1)))) return st; // bm_off
+  if ((st = g->counters.ensure(sizeof(unsigned long long) * 64))) return st;
+  if ((st = g->lb.ensure(sizeof(LbState) * 8))) return st;
+  size_t tmp_scan = 0, tmp_sort = 0, tmp_scan2 = 0;
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, g->outdeg.as<int32_t>(),
+                                        g->dag_off.as<int64_t>(), (int)(n + 1), s));
+  WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+      nullptr, tmp_sort, g->keys_in.as<uint32_t>(), g->keys_out.as<uint32_t>(),
+      g->vals_in.as<int32_t>(), g->vals_out.as<int32_t>(), (int)n, 0, 32, s));
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan2, g->hist.as<unsigned long long>(),
+                                        g->table.as<unsigned long long>(), (int)(n + 1), s));
+  size_t tmp = tmp_scan > tmp_sort ? tmp_scan : tmp_sort;
+  if (tmp_scan2 > tmp) tmp = tmp_scan2;
+  if ((st = g->cub_tmp.ensure(tmp))) return st;
+
+  cudaEvent_t e0, e1, k0, k1;
+  WM_CUDA(cudaEventCreate(&e0));
+  WM_CUDA(cudaEventCreate(&e1));
+  WM_CUDA(cudaEventCreate(&k0));
+  WM_CUDA(cudaEventCreate(&k1));
+  WM_CUDA(cudaEventRecord(e0, s));
+  unsigned long long *ctr = g->counters.as<unsigned long long>();
+  WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
+  const int tpb = 256;
+  const int vblocks = (int)((n * 32 + tpb - 1) / tpb < (int64_t)g->num_sms * 64
+                                ? (n * 32 + tpb - 1) / tpb
+                                : (int64_t)g->num_sms * 64);
+  orient_count_kernel<<<vblocks, tpb, 0, s>>>(n, g->offsets, g->neighbors, order,
+                                              g->outdeg.as<int32_t>());
+  WM_CUDA(cudaMemsetAsync(g->outdeg.as<int32_t>() + n, 0, sizeof(int32_t), s));
+  size_t tb = g->cub_tmp.bytes;
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.ptr, tb, g->outdeg.as<int32_t>(),
+                                        g->dag_off.as<int64_t>(), (int)(n + 1), s));
+  orient_fill_kernel<<<vblocks, tpb, 0, s>>>(n, g->offsets, g->neighbors, order,
+                                             g->dag_off.as<int64_t>(), g->dag_nbr.as<int32_t>());
+  const int64_t rb = cfg->root_begin < 0 ? 0 : cfg->root_begin;
+  const int64_t re = (cfg->root_end < 0 || cfg->root_end > n) ? n : cfg->root_end;
+  const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
+                                ? (n + tpb - 1) / tpb
+                                : (int64_t)g->num_sms * 16);
+  task_keys_kernel<<<eblocks, tpb, 0, s>>>(n, g->outdeg.as<int32_t>(), k, rb, re,
+                                           g->keys_in.as<uint32_t>(), g->vals_in.as<int32_t>());
+  tb = g->cub_tmp.bytes;
+  WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+      g->cub_tmp.ptr, tb, g->keys_in.as<uint32_t>(), g->keys_out.as<uint32_t>(),
+      g->vals_in.as<int32_t>(), g->vals_out.as<int32_t>(), (int)n, 0, 32, s));
+  bucket_count_kernel<<<eblocks, tpb, 0, s>>>(n, g->keys_out.as<uint32_t>(), ctr + 8);
+  unsigned long long hb[8];
+  WM_CUDA(cudaMemcpyAsync(hb, ctr + 8, sizeof hb, cudaMemcpyDeviceToHost, s));
+  WM_CUDA(cudaStreamSynchronize(s));
+  res->launches = 5;
+  if (hb[6]) {
+    return fail(WM_ECAPACITY,
+                "%llu root(s) have more than 1024 out-neighbours under this orientation "
+                "(use order=degree)", hb[6]);
+  }
+  unsigned long long ntask = 0;
+  for (int c = 0; c < 6; ++c) ntask += hb[c];
+  // bitmap arena offsets: exclusive scan of d * ceil(d/32) over the sorted tasks
+  unsigned long long *words = g->hist.as<unsigned long long>();
+  unsigned long long *bm_off = g->table.as<unsigned long long>();
+  unsigned long long arena_words = 0;
+  if (ntask) {
+    task_words_kernel<<<eblocks, tpb, 0, s>>>(ntask, g->keys_out.as<uint32_t>(), words);
+    WM_CUDA(cudaMemsetAsync(words + ntask, 0, sizeof(unsigned long long), s));
+    tb = g->cub_tmp.bytes;
+    WM_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.ptr, tb, words, bm_off, (int)(ntask + 1), s));
+    WM_CUDA(cudaMemcpyAsync(&arena_words, bm_off + ntask, sizeof arena_words,
+                            cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaStreamSynchronize(s));
+    res->launches += 1;
+  }
+  if ((st = g->arena.ensure(sizeof(uint32_t) * (arena_words + 1)))) return st;
+  LbState *lbs = g->lb.as<LbState>();
+  int max_w = 0;
+  double idle_w = 0, idle_tail_w = 0, tot_w = 0;
+  int launched = 0;
+  WM_CUDA(cudaEventRecord(k0, s));
+  // buckets are contiguous in the descending sort: W=32 first.  Build all
+  // bitmaps first, then enumerate.
+  for (int pass = 0; pass < 2; ++pass) {
+    unsigned long long begin = 0;
+    for (int c = 5; c >= 0; --c) {
+      const unsigned long long cnt = hb[c];
+      if (!cnt) continue;
+      const int W = 1 << c;
+      CliqueArgs a;
+      a.doff = g->dag_off.as<int64_t>();
+      a.dnbr = g->dag_nbr.as<int32_t>();
+      a.tasks = g->vals_out.as<int32_t>() + begin;
+      a.bm_off = bm_off + begin;
+      a.bm = g->arena.as<uint32_t>();
+      a.task_offset = (unsigned long long)cfg->shard_rank;
+      a.task_stride = (unsigned long long)cfg->shard_count;
+      a.ntasks =
+          cnt > a.task_offset ? (cnt - a.task_offset + a.task_stride - 1) / a.task_stride : 0;
+      a.k = k;
+      a.lb_on = lb_on;
+      a.lb_poll = cfg->lb_poll > 0 ? cfg->lb_poll : 1;
+      a.idle_min = 1;
+      a.L.lb = lbs + launched;
+      a.counters = ctr;
+      begin += cnt;
+      if (!a.ntasks) continue;
+      if (pass == 0) {
+        // only this shard's tasks need bitmaps, but building the bucket's
+        // full set keeps the offsets shard-independent; cheap next to the DFS
+        switch (c) {
+#define WM_BCASE(CC, WW) \
+  case CC:               \
+    st = launch_build<WW>(g, a, cnt, s); \
+    break;
+          WM_BCASE(0, 1) WM_BCASE(1, 2) WM_BCASE(2, 4) WM_BCASE(3, 8) WM_BCASE(4, 16)
+          WM_BCASE(5, 32)
+#undef WM_BCASE
+        }
+        if (st) return st;
+        res->launches += 1;
+        continue;
+      }
+      int warps = 0;
+      switch (c) {
+#define WM_CASE(CC, WW)                                                      \
+  case CC:                                                                   \
+    st = bytes ? launch_enum<WW, true>(g, cfg, a, s, &warps)                 \
+               : launch_enum<WW, false>(g, cfg, a, s, &warps);               \
+    break;
+        WM_CASE(0, 1) WM_CASE(1, 2) WM_CASE(2, 4) WM_CASE(3, 8) WM_CASE(4, 16) WM_CASE(5, 32)
+#undef WM_CASE
+      }
+      if (st) return st;
+      if (W > max_w) max_w = W;
+      if (warps > res->warps) res->warps = warps;
+      res->launches += 2;
+      ++launched;
+    }
+  }
+  WM_CUDA(cudaEventRecord(k1, s));
+  unsigned long long hc[8];
+  WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
+  LbState hl[8];
+  if (launched)
+    WM_CUDA(cudaMemcpyAsync(hl, lbs, sizeof(LbState) * launched, cudaMemcpyDeviceToHost, s));
+  WM_CUDA(cudaEventRecord(e1, s));
+  WM_CUDA(cudaStreamSynchronize(s));
+  float kms = 0, dms = 0;
+  WM_CUDA(cudaEventElapsedTime(&kms, k0, k1));
+  WM_CUDA(cudaEventElapsedTime(&dms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaEventDestroy(k0);
+  cudaEventDestroy(k1);
+  res->clique_count = hc[0];
+  res->leaves = hc[0];
+  res->alg_bytes = bytes ? hc[1] : 0;
+  res->tasks = hc[2];
+  res->nodes = hc[3];
+  res->polls = hc[4];
+  res->kernel_ms = kms;
+  res->device_ms = dms;
+  res->bucket_words = max_w;
+  for (int i = 0; i < launched; ++i) {
+    wm_result tmp = {};
+    finish_lb_stats(hl[i], &tmp);
+    const double span = (double)(hl[i].t_end_max - hl[i].t_start_min) * hl[i].total_warps;
+    if (hl[i].t_end_max > hl[i].t_start_min) {
+      idle_w += tmp.idle_warp_fraction * span;
+      idle_tail_w += tmp.idle_warp_fraction_tail * span;
+      tot_w += span;
+    }
+    res->migrations += tmp.migrations;
+    res->rebalance_count += tmp.rebalance_count;
+    if (hl[i].error) return fail(hl[i].error, "device raised status %d", hl[i].error);
+  }
+  res->idle_warp_fraction = tot_w > 0 ? idle_w / tot_w : 0;
+  res->idle_warp_fraction_tail = tot_w > 0 ? idle_tail_w / tot_w : 0;
+  res->peak_ext = (uint64_t)max_w * 32;
+  return WM_OK;
+}
+
+}  // namespace wm

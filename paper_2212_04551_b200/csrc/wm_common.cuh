@@ -1,0 +1,315 @@
+// wm_common.cuh — shared device/host plumbing for libwm_b200.so.
+//
+// * error capture for the C-ABI (wm_last_error)
+// * warp primitives (ballot/popc compaction, reductions)
+// * the on-device load balancer.  It replaces the reference's host-side
+//   Coordinator (pkg/src/warpmine/balance.py:163-194), which stops every warp
+//   at a consistent state and hands one pending extension to each idle warp
+//   in order (balance.py:80-128).  On the device it is a ticketed rendezvous
+//   ring that needs only fetch-and-add (no CAS retry loops):
+//     - a warp whose stack is empty and finds the root cursor drained takes an
+//       idle ticket t = FAA(tail) and spins on slot t of the ring (its own
+//       line: thousands of idle warps cost no shared traffic);
+//     - busy warps poll (tail - head) every `poll` DFS steps; when
+//       active/total < threshold (balance.py:63-66) a busy warp takes a donor
+//       ticket h = FAA(head) and writes its donation record into slot h —
+//       tickets pair donors and idle warps FIFO, like the reference's
+//       round-robin over the idle list, and nobody is ever stopped;
+//     - `active` counts busy warps plus records in flight, so active == 0 is a
+//       stable termination condition.
+//   This is the paper's stated future work: balancing
+//   without stopping and relaunching the kernel.
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <string>
+#include <cuda_runtime.h>
+#include <cuda/atomic>
+
+#include "../../include/warpmine_b200.h"
+
+namespace wm {
+
+// ---------------------------------------------------------------------------
+// error capture
+
+void set_error(const std::string &msg);
+int fail(int code, const char *fmt, ...);
+
+#define WM_CUDA(call)                                                        \
+  do {                                                                       \
+    cudaError_t _e = (call);                                                 \
+    if (_e != cudaSuccess)                                                   \
+      return ::wm::fail(WM_ECUDA, "%s failed at %s:%d: %s", #call, __FILE__, \
+                        __LINE__, cudaGetErrorString(_e));                   \
+  } while (0)
+
+// ---------------------------------------------------------------------------
+// device helpers
+
+constexpr int kWarp = 32;
+constexpr int kMaxK = 12;
+constexpr int kSlotWords = 128;  // ring slot: [0] seq (ticket+1), [32..127] record
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ uint64_t globaltimer_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// first index in sorted a[0..n) with a[i] >= x (shared or global)
+template <typename T>
+__device__ __forceinline__ int lower_bound_i(const T *a, int n, T x) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    int mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// membership of x in the ascending CSR row [b, e) of nbr (global, read-only)
+__device__ __forceinline__ bool row_contains(const int32_t *__restrict__ nbr, int64_t b,
+                                             int64_t e, int32_t x) {
+  while (b < e) {
+    int64_t mid = (b + e) >> 1;
+    int32_t y = __ldg(nbr + mid);
+    if (y == x) return true;
+    if (y < x) b = mid + 1; else e = mid;
+  }
+  return false;
+}
+
+using aref_u64 = cuda::atomic_ref<unsigned long long, cuda::thread_scope_device>;
+using aref_i32 = cuda::atomic_ref<int, cuda::thread_scope_device>;
+using aref_u32 = cuda::atomic_ref<uint32_t, cuda::thread_scope_device>;
+
+// ---------------------------------------------------------------------------
+// load-balancing state (one per enumeration launch); hot fields on their own
+// 128-byte lines so polls never queue behind another field's atomics
+
+struct alignas(128) LbState {
+  alignas(128) unsigned long long task_cursor;  // next root task (engine.py:187 deque)
+  alignas(128) int active;                      // busy warps + records in flight
+  int total_warps;
+  alignas(128) unsigned long long head;         // donor tickets
+  alignas(128) unsigned long long tail;         // idle-warp tickets
+  alignas(128) unsigned long long migrations;   // donated prefixes (balance.py:192-193)
+  unsigned long long donation_polls;            // donations made (rebalance_count)
+  // t_base is the globaltimer at lb_init; every other time is relative to it
+  // (absolute ns summed over thousands of warps would overflow u64)
+  unsigned long long t_base, t_start_min, t_end_max, t_tail_min;
+  unsigned long long sum_start, sum_end, sum_idle_ns, sum_tail_idle_ns;
+  unsigned long long peak_ext;
+  int error;                                    // WM_E* raised on device
+};
+
+struct LbShared {
+  LbState *lb;
+  uint32_t *ring;     // [cap * kSlotWords]
+  uint32_t cap;       // power of two >= 2 * warps
+  uint32_t words;     // record words (<= 96)
+};
+
+__device__ __forceinline__ unsigned long long ld_relaxed(unsigned long long *p) {
+  return aref_u64(*p).load(cuda::std::memory_order_relaxed);
+}
+__device__ __forceinline__ int ld_relaxed(int *p) {
+  return aref_i32(*p).load(cuda::std::memory_order_relaxed);
+}
+
+__device__ __forceinline__ void raise_error(LbState *lb, int code) {
+  atomicCAS(&lb->error, 0, code);
+}
+
+// A record is up to 96 u32 held lane-distributed: lane l holds word 32r+l in w[r].
+struct Rec3 {
+  uint32_t w[3];
+};
+
+// word `idx` of a lane-distributed record (warp-collective; idx may differ per lane)
+__device__ __forceinline__ uint32_t rec_word(const Rec3 &r, int idx) {
+  const int src = idx & 31, reg = (idx >> 5) & 3;
+  const uint32_t a = __shfl_sync(0xffffffffu, r.w[0], src);
+  const uint32_t b = __shfl_sync(0xffffffffu, r.w[1], src);
+  const uint32_t c = __shfl_sync(0xffffffffu, r.w[2], src);
+  return reg == 0 ? a : (reg == 1 ? b : c);
+}
+
+__global__ void lb_init_kernel(LbState *lb, int total_warps, uint32_t *ring, uint32_t cap);
+
+// Donor side: write `rec` into the next donor ticket's slot.  Warp-collective.
+// Only called after donation_wanted() saw waiting idle tickets; a rare
+// overshoot (two donors racing for one waiting warp) leaves the record for
+// the next warp that goes idle — possibly the donor itself.
+__device__ __forceinline__ void donate_record(const LbShared &L, const Rec3 &rec) {
+  const int lane = lane_id();
+  unsigned long long h = 0;
+  if (lane == 0) {
+    atomicAdd(&L.lb->active, 1);  // the record is work in flight
+    h = atomicAdd(&L.lb->head, 1ull);
+  }
+  h = __shfl_sync(0xffffffffu, h, 0);
+  uint32_t *slot = L.ring + (size_t)(h & (L.cap - 1)) * kSlotWords;
+  if (lane == 0) {
+    // slot reuse guard: the record of ticket h - cap must have been consumed
+    // (cap >= 8 x warps makes this wait practically never taken)
+    while (aref_u32(slot[0]).load(cuda::std::memory_order_acquire) != 0u) __nanosleep(64);
+  }
+  __syncwarp();
+#pragma unroll
+  for (int r = 0; r < 3; ++r)
+    if ((uint32_t)(lane + 32 * r) < L.words) __stcg(slot + 32 + 32 * r + lane, rec.w[r]);
+  __threadfence();
+  __syncwarp();
+  if (lane == 0) aref_u32(slot[0]).store((uint32_t)(h + 1), cuda::std::memory_order_release);
+}
+
+// Per-warp bookkeeping of idle time (for idle_warp_fraction).
+struct WarpClock {
+  unsigned long long t_start, idle_ns, tail_idle_ns;
+};
+
+// Warp-collective work acquisition shared by the clique and motif kernels.
+//   returns 1: root task (task index in *task_idx)
+//           2: donated record (lane-distributed in rec)
+//           0: no work left — exit
+// `roots_left` is warp-uniform state owned by the caller.
+__device__ __forceinline__ int acquire_work(const LbShared &L, bool lb_on,
+                                            unsigned long long ntasks, bool &roots_left,
+                                            unsigned long long &task_idx, Rec3 &rec,
+                                            WarpClock &clk) {
+  const int lane = lane_id();
+  LbState *lb = L.lb;
+  if (roots_left) {
+    unsigned long long idx = 0;
+    if (lane == 0) idx = atomicAdd(&lb->task_cursor, 1ull);
+    idx = __shfl_sync(0xffffffffu, idx, 0);
+    if (idx < ntasks) {
+      task_idx = idx;
+      return 1;
+    }
+    roots_left = false;
+    if (lane == 0) {
+      const unsigned long long ta = globaltimer_ns(), base = lb->t_base;
+      atomicMin(&lb->t_tail_min, ta > base ? ta - base : 0ull);
+    }
+  }
+  if (!lb_on) return 0;
+  const unsigned long long t0 = globaltimer_ns();
+  unsigned long long t = 0;
+  if (lane == 0) {
+    t = atomicAdd(&lb->tail, 1ull);
+    atomicSub(&lb->active, 1);
+  }
+  t = __shfl_sync(0xffffffffu, t, 0);
+  uint32_t *slot = L.ring + (size_t)(t & (L.cap - 1)) * kSlotWords;
+  unsigned backoff = 32;
+  int result = 0;
+  for (;;) {
+    int state = 0;  // 1 record, 2 exit
+    if (lane == 0) {
+      if (aref_u32(slot[0]).load(cuda::std::memory_order_acquire) == (uint32_t)(t + 1)) state = 1;
+      else if (ld_relaxed(&lb->active) <= 0 || ld_relaxed(&lb->error)) state = 2;
+    }
+    state = __shfl_sync(0xffffffffu, state, 0);
+    if (state == 1) {
+      __threadfence();
+#pragma unroll
+      for (int r = 0; r < 3; ++r)
+        if ((uint32_t)(lane + 32 * r) < L.words) rec.w[r] = __ldcg(slot + 32 + 32 * r + lane);
+      __syncwarp();
+      if (lane == 0) aref_u32(slot[0]).store(0u, cuda::std::memory_order_release);
+      result = 2;
+      break;
+    }
+    if (state == 2) { result = 0; break; }
+    __nanosleep(backoff);
+    if (backoff < 1024) backoff <<= 1;
+  }
+  const unsigned long long dt = globaltimer_ns() - t0;
+  clk.idle_ns += dt;
+  clk.tail_idle_ns += dt;
+  return result;
+}
+
+__device__ __forceinline__ void warp_clock_begin(WarpClock &clk, LbState *lb) {
+  const unsigned long long base = lb->t_base;
+  const unsigned long long t = globaltimer_ns();
+  clk.t_start = t > base ? t - base : 0ull;
+  clk.idle_ns = 0;
+  clk.tail_idle_ns = 0;
+}
+
+__device__ __forceinline__ void warp_clock_end(LbState *lb, const WarpClock &clk) {
+  if (lane_id() == 0) {
+    const unsigned long long base = lb->t_base;
+    const unsigned long long ta = globaltimer_ns();
+    const unsigned long long t = ta > base ? ta - base : 0ull;
+    atomicMin(&lb->t_start_min, clk.t_start);
+    atomicMax(&lb->t_end_max, t);
+    atomicAdd(&lb->sum_start, clk.t_start);
+    atomicAdd(&lb->sum_end, t);
+    atomicAdd(&lb->sum_idle_ns, clk.idle_ns);
+    atomicAdd(&lb->sum_tail_idle_ns, clk.tail_idle_ns);
+  }
+}
+
+// Should a busy warp donate now?  balance.py:63-66: rebalance when
+// active/total < threshold  <=>  idle > total * (1 - threshold); idle =
+// idle tickets not yet served by a donor ticket.
+__device__ __forceinline__ bool donation_wanted(const LbShared &L, int idle_min) {
+  int want = 0;
+  if (lane_id() == 0) {
+    const unsigned long long t = ld_relaxed(&L.lb->tail);
+    const unsigned long long h = ld_relaxed(&L.lb->head);
+    want = (long long)(t - h) >= (long long)idle_min;
+  }
+  return __shfl_sync(0xffffffffu, want, 0) != 0;
+}
+
+// ---------------------------------------------------------------------------
+// host-side helpers
+
+struct DeviceBuffer {
+  void *ptr = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t want);
+  void release();
+  ~DeviceBuffer() { release(); }
+  template <typename T> T *as() const { return static_cast<T *>(ptr); }
+};
+
+struct Graph {
+  int64_t n = 0, nnz = 0;
+  int64_t max_degree = 0;
+  int device = 0;
+  int num_sms = 0;
+  int64_t *offsets = nullptr;   // device [n+1]
+  int32_t *neighbors = nullptr; // device [nnz]
+  cudaStream_t own_stream = nullptr;
+  // scratch (grow-only, reused across runs)
+  DeviceBuffer dag_off, dag_nbr, outdeg, keys_in, keys_out, vals_in, vals_out, cub_tmp;
+  DeviceBuffer lb, ring, counters, hist, arena, table, pub;
+};
+
+// Allocates the balancer's ring for `warps` and initialises lb (one
+// LbState) on stream s.
+int lb_prepare(Graph *g, LbState *lb, int warps, uint32_t words, LbShared *out, cudaStream_t s);
+
+int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s);
+int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s);
+
+// fills the idle fractions and LB stats of `res` from a device LbState copy
+void finish_lb_stats(const LbState &h, wm_result *res);
+
+}  // namespace wm

@@ -1,0 +1,72 @@
+"""Multi-GPU plumbing: root-task sharding and the single count allreduce.
+
+The path shards naturally: root subtrees are independent
+(reference ``engine.py:187``, ``:809-816``) and results are plain sums
+(``engine.py:821-826``, ``aggregate.py:39-55``).  One process per GPU;
+rank ``r`` of ``N`` takes the cost-sorted root tasks ``i ≡ r (mod N)``
+(computed identically on every rank inside ``wm_run``), runs its own
+on-device load balancer, and the ranks combine
+``[clique_count, leaves, alg_bytes, hist[P]]`` with ONE
+``all_reduce(SUM)`` over NCCL (gloo on CPU for the host-logic tests).
+"""
+
+from __future__ import annotations
+
+from dataclasses import replace
+
+
+def _dist():
+    try:
+        import torch.distributed as dist
+    except ImportError:  # pragma: no cover
+        return None
+    return dist if dist.is_available() and dist.is_initialized() else None
+
+
+def default_shard():
+    """(rank, world) of the initialised process group, else (0, 1)."""
+    dist = _dist()
+    if dist is None:
+        return (0, 1)
+    return (dist.get_rank(), dist.get_world_size())
+
+
+def shard_tasks(tasks, rank: int, count: int):
+    """Host restatement of the device's cyclic task split (for tests)."""
+    return list(tasks)[rank::count]
+
+
+def pack(res) -> list:
+    hist = res.pattern_counts or []
+    return [res.clique_count or 0, res.aggregated_total, res.alg_bytes, res.migrations,
+            res.rebalance_count, res.tasks] + list(hist)
+
+
+def allreduce_result(res, group=None, device=None):
+    """Sum the counters of every rank (one all_reduce).  Timing fields are
+    max-reduced in a second tiny collective so ``kernel_ms`` is the job's
+    critical path."""
+    import torch
+    dist = _dist()
+    if dist is None:
+        return res
+    backend = dist.get_backend(group)
+    if device is None:
+        device = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" \
+            else torch.device("cpu")
+    vals = torch.tensor(pack(res), dtype=torch.int64, device=device)
+    dist.all_reduce(vals, op=dist.ReduceOp.SUM, group=group)
+    t = torch.tensor([res.kernel_ms, res.device_ms, res.wall_seconds,
+                      res.idle_warp_fraction, res.idle_warp_fraction_tail],
+                     dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    v = [int(x) for x in vals.tolist()]
+    tt = t.tolist()
+    return replace(res,
+                   clique_count=v[0] if res.clique_count is not None else None,
+                   aggregated_total=v[1], alg_bytes=v[2], migrations=v[3],
+                   rebalance_count=v[4], tasks=v[5],
+                   pattern_counts=v[6:] if res.pattern_counts is not None else None,
+                   kernel_ms=tt[0], device_ms=tt[1], wall_seconds=tt[2],
+                   idle_warp_fraction=tt[3], idle_warp_fraction_tail=tt[4],
+                   devices=dist.get_world_size(group))
