@@ -1,0 +1,96 @@
+"""GPU parity: k-motif pattern histograms (motif_app) through the C-ABI vs the
+reference's own results (golden vectors) and the validated CPU restatement."""
+
+from __future__ import annotations
+
+import pytest
+
+from conftest import dictionary, golden_cases, graph_from_entry
+
+pytestmark = pytest.mark.gpu
+
+
+def _cases(golden):
+    cache = {}
+    for e, r in golden_cases(golden, app="motif"):
+        if e["name"] not in cache:
+            cache[e["name"]] = graph_from_entry(e)
+        yield cache[e["name"]], e, r
+
+
+@pytest.mark.parametrize("mode", ["wc", "opt"])
+def test_motif_histograms_match_reference(golden, cuda, mode):
+    from paper_2212_04551_b200 import BalanceConfig, run_motifs
+    bad = []
+    n = 0
+    for g, e, r in _cases(golden):
+        kw = {}
+        if mode == "opt":
+            kw["balance_config"] = BalanceConfig(threshold=1.0, poll_interval=1)
+        res = run_motifs(g, r["k"], dictionary(r["k"]), mode=mode, **kw)
+        n += 1
+        if res.pattern_counts != r["hist"] or res.aggregated_total != r["leaves"]:
+            bad.append((e["name"], r["k"], res.pattern_counts, r["hist"]))
+    assert n > 100
+    assert not bad, bad[:5]
+
+
+def test_motif_alg_bytes_match_reference(golden, cuda):
+    from paper_2212_04551_b200 import run_motifs
+    for g, e, r in _cases(golden):
+        res = run_motifs(g, r["k"], dictionary(r["k"]), count_bytes=True)
+        assert res.alg_bytes == r["alg_bytes"], (e["name"], r["k"], res.alg_bytes, r["alg_bytes"])
+
+
+def test_known_answers(cuda):
+    """Reference tests/test_apps.py:57-72."""
+    from paper_2212_04551_b200 import CsrGraph, complete_graph, motif_counting, path_graph
+    g1 = CsrGraph.from_edges(5, [(0, 1), (0, 2), (1, 2), (1, 3), (2, 3), (3, 4)])
+    assert motif_counting(g1, 3, dictionary(3)) == {0: 4, 1: 2}
+    assert motif_counting(path_graph(4), 3, dictionary(3)) == {0: 2, 1: 0}
+    assert motif_counting(complete_graph(4), 3, dictionary(3)) == {0: 0, 1: 4}
+
+
+@pytest.mark.parametrize("k", [3, 4, 5, 6, 7])
+def test_cross_app_identity(cuda, k):
+    """clique(k) == motif_hist(k)[last] (reference test_apps.py:85-88)."""
+    from paper_2212_04551_b200 import clique_counting, gnp_random_graph, motif_counting
+    g = gnp_random_graph(60, 0.3, 5)
+    hist = motif_counting(g, k, dictionary(k))
+    assert hist[max(hist)] == clique_counting(g, k)
+
+
+def test_forced_rebalance_conserves(golden, cuda):
+    from paper_2212_04551_b200 import BalanceConfig, run_motifs, star_of_cliques
+    g = star_of_cliques(6, 7)
+    want = golden["forced_rebalance_star_of_cliques_6_7"]["motif_4"]["hist"]
+    r = run_motifs(g, 4, dictionary(4), mode="opt",
+                   balance_config=BalanceConfig(threshold=1.0, poll_interval=1))
+    assert r.pattern_counts == want
+
+
+def test_cfg_scale_histograms(scale_golden, cuda):
+    """cfg1/cfg2 motif k=5,6 vs the pinned restatement."""
+    from paper_2212_04551_b200 import BalanceConfig, run_motifs, synth
+    for name in ("cfg1", "cfg2"):
+        g = synth.config_graph(name)
+        for k, want in scale_golden[name]["motif"].items():
+            k = int(k)
+            for mode in ("wc", "opt"):
+                kw = {"balance_config": BalanceConfig(threshold=1.0)} if mode == "opt" else {}
+                r = run_motifs(g, k, dictionary(k), mode=mode, **kw)
+                assert r.pattern_counts == want["hist"], (name, k, mode)
+
+
+def test_root_suffix_and_shards(cuda):
+    """Root suffix == induced suffix graph; cyclic shards sum to the total."""
+    from paper_2212_04551_b200 import gnp_random_graph, run_motifs
+    g = gnp_random_graph(150, 0.06, 11)
+    d = dictionary(5)
+    full = run_motifs(g, 5, d).pattern_counts
+    for r0 in (0, 40, 100):
+        a = run_motifs(g, 5, d, roots=(r0, g.n)).pattern_counts
+        b = run_motifs(g.induced_suffix(r0), 5, d).pattern_counts
+        assert a == b
+    parts = [run_motifs(g, 5, d, shard=(r, 3), reduce=False).pattern_counts for r in range(3)]
+    assert [sum(x) for x in zip(*parts)] == full
