@@ -104,7 +104,10 @@ typedef struct {
   uint64_t launches;            /* kernels launched by this call */
   uint64_t nodes;               /* internal search-tree nodes expanded */
   uint64_t polls;               /* idle-counter polls by busy warps (opt) */
+  uint64_t h2d_bytes;           /* host->device bytes copied by this call */
+  uint64_t d2h_bytes;           /* device->host bytes copied by this call */
   double kernel_ms;             /* enumeration kernel(s), CUDA events */
+  double build_ms;              /* per-root bitmap build kernels (clique) */
   double device_ms;             /* whole call on the device incl. preprocessing */
   double idle_warp_fraction;    /* idle warp-time / (warps * kernel time) */
   double idle_warp_fraction_tail; /* same, from the first root-queue drain */

@@ -55,7 +55,9 @@ class WmResult(ctypes.Structure):
                 ("pattern_counts", ctypes.POINTER(ctypes.c_uint64)),
                 ("tasks", ctypes.c_uint64), ("launches", ctypes.c_uint64),
                 ("nodes", ctypes.c_uint64), ("polls", ctypes.c_uint64),
-                ("kernel_ms", ctypes.c_double), ("device_ms", ctypes.c_double),
+                ("h2d_bytes", ctypes.c_uint64), ("d2h_bytes", ctypes.c_uint64),
+                ("kernel_ms", ctypes.c_double), ("build_ms", ctypes.c_double),
+                ("device_ms", ctypes.c_double),
                 ("idle_warp_fraction", ctypes.c_double),
                 ("idle_warp_fraction_tail", ctypes.c_double),
                 ("warps", ctypes.c_int), ("bucket_words", ctypes.c_int)]

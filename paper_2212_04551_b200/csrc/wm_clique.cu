@@ -14,21 +14,23 @@
 //   C_L = { e in N(tr[0]) : e above tr[L-1], e adjacent to tr[0..L) }
 // which, since the filters are conjunctive, equals C_{L-1} ∩ N+(tr[L-1])
 // with N+ the out-neighbours of an orientation ("lower" = above in the
-// order).  Per root task the warp stages N+(root) in shared memory and builds
-// the induced DAG among those d vertices as a d x d bitmap (sorted-set
-// intersections of N+(u_i) against N+(root), binary search in smem).  Every
-// later extension is then one W-word AND (extend + lower + clique fused),
-// compaction is implicit in the bitmap, and the last two levels are
-// aggregated in bulk: sum over j in C of popc(C & A[j]) — each lane takes one
-// member j (ballot-free: lane l owns bit l of every word).  Counts are
-// orientation-invariant; WM_ORDER_ID reproduces the
-// reference's id order exactly, WM_ORDER_DEGREE bounds d by the degeneracy.
+// order).  A preprocessing kernel builds, once per root, the induced DAG on
+// the d = |N+(root)| candidates as a d x d bitmap (sorted-set intersections
+// of N+(u_i) against N+(root) by binary search in shared memory) into an HBM
+// arena.  Every later extension is one W-word AND (extend + lower + clique
+// fused), compaction is implicit in the bitmap, and the last three levels are
+// aggregated in bulk: for a node at traversal length k-3 with candidates C,
+//   leaves = sum_{j in C} sum_{l in C&A[j]} popc(C & A[j] & A[l])
+// with one lane per j (k = 3 uses the two-level form sum_j popc(C & A[j])).
+// Counts are orientation-invariant; WM_ORDER_ID
+// reproduces the reference's id order exactly, WM_ORDER_DEGREE bounds d by
+// the degeneracy.
 //
 // Work distribution: persistent warps pull root tasks (cost-sorted, largest
 // first) from a global cursor (the engine's root deque, engine.py:187).  In
-// opt mode busy warps poll the idle-warp counter and donate their shallowest
-// pending extension (balance.py:102-155 semantics: the thief owns exactly the
-// stolen branch; inherited levels are never regenerated).
+// opt mode busy warps poll the idle-warp ring and donate half of their
+// shallowest pending extensions (balance.py:102-155 semantics: the thief owns
+// exactly the stolen branches; inherited levels are never regenerated).
 #include <cub/cub.cuh>
 
 #include "wm_common.cuh"
@@ -222,88 +224,146 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
 
 // --------------------------------------------------------------------------
 // 2) enumeration: per-warp DFS-wide stack in shared memory
+//
+// One launch per width class WMAX (4, 8, 16, 32).  The class-4 launch runs
+// every task with d <= 128; each task is processed by the instantiation for
+// its own word count (1, 2 or 4) over a shared per-warp buffer, so small
+// roots pay for narrow rows only.
 
-template <int W> struct CliqueSmem {
-  static constexpr int D = 32 * W;                // max local vertices
-  static constexpr int S = (W == 1) ? 1 : W + 1;  // odd row stride: conflict-free bulk reads
-  uint32_t adj[D * S];                            // local DAG rows of the current root
-  uint32_t C[kMaxK][W];                           // candidate set per level
-  uint32_t P[kMaxK][W];                           // unconsumed members per level
-  unsigned long long below[kMaxK];                // leaves under the level's node (B_alg)
-  int32_t last[kMaxK];                            // vertex appended at the level
+template <int WMAX> struct CliqueSmem {
+  static constexpr int D = 32 * WMAX;
+  static constexpr int S = (WMAX == 1) ? 1 : WMAX + 1;
+  uint32_t adj[D * S];                 // local DAG rows, stride w+1 (odd) for width w
+  uint32_t C[kMaxK * WMAX];            // candidate set per level  [s * w + x]
+  uint32_t P[kMaxK * WMAX];            // unconsumed members       [s * w + x]
+  unsigned long long below[kMaxK];     // leaves under the level's node (B_alg)
+  int32_t last[kMaxK];                 // vertex appended at the level
 };
 
 struct CliqueArgs {
   const int64_t *doff;
   const int32_t *dnbr;
-  const int32_t *tasks;           // bucket's cost-sorted roots
-  const unsigned long long *bm_off;  // bucket's bitmap offsets (per task)
-  const uint32_t *bm;             // bitmap arena
-  unsigned long long ntasks;      // tasks of this shard in the bucket
-  unsigned long long task_offset; // shard rank
-  unsigned long long task_stride; // shard count
+  const int32_t *tasks;              // class's cost-sorted roots
+  const unsigned long long *bm_off;  // class's bitmap offsets (per task)
+  const uint32_t *bm;                // bitmap arena
+  unsigned long long ntasks;         // tasks of this shard in the class
+  unsigned long long task_offset;    // shard rank
+  unsigned long long task_stride;    // shard count
   int k;
   int lb_on;
   int lb_poll;
   int idle_min;
   LbShared L;
-  unsigned long long *counters;   // [0] cliques [1] B_alg [2] tasks [3] nodes [4] polls
+  unsigned long long *counters;      // [0] cliques [1] B_alg [2] tasks [3] nodes [4] polls
 };
 
-// Leaves under a node at traversal length k-2 with candidate set C[s]:
-// for each member j (lane l owns bit l of each word) popc(C & A[j]).
-// Returns this lane's partial; with BYTES also adds B_alg of the length-(k-1)
-// nodes and returns the warp total in `warp_total`.
-template <int W, bool BYTES>
-__device__ __forceinline__ unsigned long long bulk_count(const CliqueSmem<W> &sm, int s,
-                                                         const CliqueArgs &a, int64_t list_base,
-                                                         unsigned long long &bytes,
-                                                         unsigned long long &warp_total) {
-  constexpr int S = CliqueSmem<W>::S;
+template <int w> struct Width {
+  static constexpr int S = (w == 1) ? 1 : w + 1;
+};
+
+__device__ __forceinline__ unsigned long long outdeg_bytes(const CliqueArgs &a, int32_t u) {
+  return 4ull * (unsigned long long)(__ldg(a.doff + u + 1) - __ldg(a.doff + u));
+}
+
+// Two-level bulk (traversal length k-2, k == 3 roots): sum_j popc(C & A[j]).
+template <int w, bool BYTES>
+__device__ __forceinline__ unsigned long long bulk2(const uint32_t *adj, const uint32_t *Cs,
+                                                    const CliqueArgs &a, int64_t lb,
+                                                    unsigned long long &bytes) {
+  constexpr int S = Width<w>::S;
   const int lane = lane_id();
-  uint32_t c[W];
+  uint32_t c[w];
 #pragma unroll
-  for (int x = 0; x < W; ++x) c[x] = sm.C[s][x];
+  for (int x = 0; x < w; ++x) c[x] = Cs[x];
   unsigned long long part = 0;
 #pragma unroll
-  for (int w = 0; w < W; ++w) {
-    if (c[w] == 0u) continue;
-    if ((c[w] >> lane) & 1u) {
-      const int j = w * 32 + lane;
-      const uint32_t *row = sm.adj + j * S;
+  for (int q = 0; q < w; ++q) {
+    if (c[q] == 0u) continue;
+    if ((c[q] >> lane) & 1u) {
+      const int j = q * 32 + lane;
+      const uint32_t *row = adj + j * S;
       uint32_t t = 0;
 #pragma unroll
-      for (int x = 0; x < W; ++x) t += __popc(c[x] & row[x]);
+      for (int x = 0; x < w; ++x) t += __popc(c[x] & row[x]);
       part += t;
-      if (BYTES && t) {
-        const int32_t u = __ldg(a.dnbr + list_base + j);
-        bytes += 4ull * (unsigned long long)(__ldg(a.doff + u + 1) - __ldg(a.doff + u));
+      if (BYTES && t) bytes += outdeg_bytes(a, __ldg(a.dnbr + lb + j));
+    }
+  }
+  return part;
+}
+
+// Three-level bulk for a node at traversal length k-3 with candidates C and
+// members to expand J (J == C except for donated partial levels): one lane per
+// j in J; the lane walks the members l of Cj = C & A[j] and adds
+// popc(Cj & A[l]).  Returns this lane's partial; with BYTES, adds B_alg of the
+// productive length k-2 and k-1 nodes and reports the warp total.
+template <int w, bool BYTES>
+__device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const uint32_t *Cs,
+                                                    const uint32_t *Js, const CliqueArgs &a,
+                                                    int64_t lb, unsigned long long &bytes) {
+  constexpr int S = Width<w>::S;
+  const int lane = lane_id();
+  uint32_t c[w];
+#pragma unroll
+  for (int x = 0; x < w; ++x) c[x] = Cs[x];
+  unsigned long long part = 0;
+#pragma unroll
+  for (int q = 0; q < w; ++q) {
+    const uint32_t jw = Js[q];
+    if (jw == 0u) continue;
+    if ((jw >> lane) & 1u) {
+      const int j = q * 32 + lane;
+      const uint32_t *rj = adj + j * S;
+      uint32_t cj[w];
+      int cnt = 0;
+#pragma unroll
+      for (int x = 0; x < w; ++x) {
+        cj[x] = c[x] & rj[x];
+        cnt += __popc(cj[x]);
+      }
+      if (cnt >= 2) {
+        unsigned long long sub = 0;
+#pragma unroll
+        for (int y = 0; y < w; ++y) {
+          uint32_t m = cj[y];
+          while (m) {
+            const int l = y * 32 + __ffs(m) - 1;
+            m &= m - 1u;
+            const uint32_t *rl = adj + l * S;
+            uint32_t t = 0;
+#pragma unroll
+            for (int x = 0; x < w; ++x) t += __popc(cj[x] & rl[x]);
+            sub += t;
+            if (BYTES && t) bytes += outdeg_bytes(a, __ldg(a.dnbr + lb + l));
+          }
+        }
+        part += sub;
+        if (BYTES && sub) bytes += outdeg_bytes(a, __ldg(a.dnbr + lb + j));
       }
     }
   }
-  if (BYTES) warp_total = warp_sum_u64(part);
   return part;
 }
 
 // Donate the upper half of the pending members of the shallowest level that
 // has any (reference balance.py:102-128 steals the shallowest pending entry;
 // one record here carries half of that level so a thief gets a large
-// subtree).  Record: [task, level, C[level] (W words), donated P (W words)].
+// subtree).  Record: [task, level, C[level] (w words), donated P (w words)].
 // Subtrees estimated below ~4K nodes are not worth a move and stay.
 constexpr int kRecHdr = 2;
 
-template <int W>
-__device__ __forceinline__ void try_donate(CliqueSmem<W> &sm, const CliqueArgs &a, int s0, int s,
-                                           unsigned long long task) {
+template <int w>
+__device__ __forceinline__ void try_donate(uint32_t *C, uint32_t *P, const CliqueArgs &a, int s0,
+                                           int s, unsigned long long task) {
   const int lane = lane_id();
   int sd = -1;
   uint32_t pw = 0u;
   for (int t = s0; t <= s; ++t) {
-    const uint32_t w2 = lane < W ? sm.P[t][lane] : 0u;
+    const uint32_t w2 = lane < w ? P[t * w + lane] : 0u;
     if (__ballot_sync(0xffffffffu, w2 != 0u)) { sd = t; pw = w2; break; }
   }
   if (sd < 0) return;
-  const uint32_t cw = lane < W ? sm.C[sd][lane] : 0u;
+  const uint32_t cw = lane < w ? C[sd * w + lane] : 0u;
   const int cnt = __popc(pw);
   int pre = cnt;
 #pragma unroll
@@ -313,7 +373,7 @@ __device__ __forceinline__ void try_donate(CliqueSmem<W> &sm, const CliqueArgs &
   }
   const int total = __shfl_sync(0xffffffffu, pre, 31);
   const int csize = __reduce_add_sync(0xffffffffu, __popc(cw));
-  const int depth = a.k - 2 - sd;  // DFS levels below, bulk level included
+  const int depth = a.k - 2 - sd;  // levels below, bulk levels included
   const float est = (float)total * __powf((float)csize, (float)(depth - 1));
   if (est < 4096.f) return;
   pre -= cnt;  // exclusive prefix
@@ -331,13 +391,13 @@ __device__ __forceinline__ void try_donate(CliqueSmem<W> &sm, const CliqueArgs &
   for (int r = 0; r < 3; ++r) {
     const int idx = 32 * r + lane;
     const uint32_t cv = __shfl_sync(0xffffffffu, cw, (idx - kRecHdr) & 31);
-    const uint32_t gv = __shfl_sync(0xffffffffu, give, (idx - kRecHdr - W) & 31);
+    const uint32_t gv = __shfl_sync(0xffffffffu, give, (idx - kRecHdr - w) & 31);
     rec.w[r] = idx == 0 ? (uint32_t)task
              : idx == 1 ? (uint32_t)sd
-             : (idx - kRecHdr < W ? cv : (idx - kRecHdr - W < W ? gv : 0u));
+             : (idx - kRecHdr < w ? cv : (idx - kRecHdr - w < w ? gv : 0u));
   }
   donate_record(a.L, rec);
-  if (lane < W) sm.P[sd][lane] = pw & ~give;
+  if (lane < w) P[sd * w + lane] = pw & ~give;
   const int moved = __reduce_add_sync(0xffffffffu, __popc(give));
   if (lane == 0) {
     atomicAdd(&a.L.lb->migrations, (unsigned long long)moved);
@@ -346,18 +406,154 @@ __device__ __forceinline__ void try_donate(CliqueSmem<W> &sm, const CliqueArgs &
   __syncwarp();
 }
 
-template <int W, bool BYTES>
-__global__ void __launch_bounds__(256) clique_enum_kernel(CliqueArgs a) {
-  extern __shared__ __align__(16) unsigned char smraw[];
-  CliqueSmem<W> &sm = reinterpret_cast<CliqueSmem<W> *>(smraw)[threadIdx.x >> 5];
-  constexpr int S = CliqueSmem<W>::S;
+struct TaskCounters {
+  unsigned long long acc, bytes, nodes, polls;
+  int poll;
+};
+
+// Process one task (root or donated level) of word width w.
+template <int w, int WMAX, bool BYTES>
+__device__ __noinline__ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
+                                      unsigned long long task, int s0, int32_t root, int d,
+                                      int64_t lb, const Rec3 &rec, bool stage,
+                                      TaskCounters &tc) {
+  constexpr int S = Width<w>::S;
   const int lane = lane_id();
   const int k = a.k;
+  uint32_t *C = sm.C;
+  uint32_t *P = sm.P;
+  uint32_t *adj = sm.adj;
+  if (stage) {
+    // stage the root's rows from the arena (L2-resident) into smem
+    // (arena rows hold wv = ceil(d/32) words; words wv..w-1 of a row are
+    // never read unmasked: C is zero there)
+    const uint32_t *src = a.bm + __ldg(a.bm_off + task);
+    const int wv = (d + 31) >> 5;
+    if (w == 1) {
+      for (int i = lane; i < d; i += 32) adj[i] = __ldg(src + i);
+    } else if (wv == w) {
+      for (int i = lane; i < d * w; i += 32) {
+        const int r = i / w, x = i - r * w;
+        adj[r * S + x] = __ldg(src + i);
+      }
+    } else {
+      for (int i = lane; i < d * wv; i += 32) {
+        const int r = i / wv, x = i - r * wv;
+        adj[r * S + x] = __ldg(src + i);
+      }
+    }
+  }
+  {
+    // donated record: words 2..w+1 = C[s0], w+2..2w+1 = pending subset
+    const uint32_t cv = rec_word(rec, kRecHdr + lane);
+    const uint32_t pv = rec_word(rec, kRecHdr + w + lane);
+    if (lane < w) {
+      uint32_t cword, pword;
+      if (kind == 1) {
+        const int lo = lane * 32;
+        cword = d >= lo + 32 ? 0xffffffffu : (d > lo ? (1u << (d - lo)) - 1u : 0u);
+        pword = cword;
+      } else {
+        cword = cv;
+        pword = pv;
+      }
+      C[s0 * w + lane] = cword;
+      P[s0 * w + lane] = pword;
+    }
+  }
+  if (BYTES && lane == 0) {
+    sm.below[s0] = 0;
+    sm.last[s0] = root;
+  }
+  __syncwarp();
+  if (s0 >= k - 3) {
+    // the task itself is a bulk node
+    unsigned long long bytes = 0;
+    const unsigned long long part =
+        (s0 == k - 2) ? bulk2<w, BYTES>(adj, C + s0 * w, a, lb, bytes)
+                      : bulk3<w, BYTES>(adj, C + s0 * w, P + s0 * w, a, lb, bytes);
+    tc.acc += part;
+    if (BYTES) {
+      tc.bytes += bytes;
+      if (warp_sum_u64(part) && lane == 0) tc.bytes += outdeg_bytes(a, root);
+    }
+    return;
+  }
+  int s = s0;
+  for (;;) {
+    // move_step: next unconsumed member at level s (lowest set bit)
+    const uint32_t pw = lane < w ? P[s * w + lane] : 0u;
+    const unsigned nz = __ballot_sync(0xffffffffu, pw != 0u);
+    if (nz == 0u) {
+      if (BYTES && lane == 0) {
+        const unsigned long long b = sm.below[s];
+        if (b) {
+          tc.bytes += outdeg_bytes(a, sm.last[s]);
+          if (s > s0) sm.below[s - 1] += b;
+        }
+      }
+      __syncwarp();
+      if (s == s0) break;
+      --s;
+      continue;
+    }
+    const int wl = __ffs(nz) - 1;
+    const uint32_t word = __shfl_sync(0xffffffffu, pw, wl);
+    const int i = wl * 32 + __ffs(word) - 1;
+    if (lane == wl) P[s * w + wl] = word & (word - 1u);
+    // extend + lower + clique, fused: C_{s+1} = C_s & A[i]
+    uint32_t cw = 0u;
+    if (lane < w) {
+      cw = C[s * w + lane] & adj[i * S + lane];
+      C[(s + 1) * w + lane] = cw;
+    }
+    const int cnt = __reduce_add_sync(0xffffffffu, __popc(cw));
+    __syncwarp();
+    ++tc.nodes;
+    if (cnt >= k - s - 1) {
+      if (s + 1 == k - 3) {
+        unsigned long long bytes = 0;
+        const unsigned long long part =
+            bulk3<w, BYTES>(adj, C + (s + 1) * w, C + (s + 1) * w, a, lb, bytes);
+        tc.acc += part;
+        if (BYTES) {
+          tc.bytes += bytes;
+          const unsigned long long tot = warp_sum_u64(part);
+          if (lane == 0 && tot) {
+            tc.bytes += outdeg_bytes(a, __ldg(a.dnbr + lb + i));
+            sm.below[s] += tot;
+          }
+        }
+        __syncwarp();
+      } else {
+        ++s;
+        if (lane < w) P[s * w + lane] = cw;
+        if (BYTES && lane == 0) {
+          sm.below[s] = 0;
+          sm.last[s] = __ldg(a.dnbr + lb + i);
+        }
+        __syncwarp();
+      }
+    }
+    // on-device load balancing (opt mode): poll the idle-warp ring
+    if (!BYTES && a.lb_on && ++tc.poll >= a.lb_poll) {
+      tc.poll = 0;
+      ++tc.polls;
+      if (donation_wanted(a.L, a.idle_min)) try_donate<w>(C, P, a, s0, s, task);
+    }
+  }
+}
+
+template <int WMAX, bool BYTES>
+__global__ void __launch_bounds__(256) clique_enum_kernel(CliqueArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  CliqueSmem<WMAX> &sm = reinterpret_cast<CliqueSmem<WMAX> *>(smraw)[threadIdx.x >> 5];
+  const int lane = lane_id();
   WarpClock clk;
   warp_clock_begin(clk, a.L.lb);
   bool roots_left = true;
-  unsigned long long acc = 0, bytes = 0, tasks_done = 0, nodes = 0, polls = 0;
-  int poll = 0;
+  TaskCounters tc = {0, 0, 0, 0, 0};
+  unsigned long long tasks_done = 0;
   unsigned long long cached = ~0ull;
   for (;;) {
     unsigned long long ti = 0;
@@ -369,122 +565,33 @@ __global__ void __launch_bounds__(256) clique_enum_kernel(CliqueArgs a) {
     if (kind == 1) {
       task = a.task_offset + ti * a.task_stride;
       s0 = 1;
+      ++tasks_done;
     } else {
       task = __shfl_sync(0xffffffffu, rec.w[0], 0);
       s0 = (int)__shfl_sync(0xffffffffu, rec.w[0], 1);
     }
     const int32_t root = __ldg(a.tasks + task);
-    const int64_t list_base = __ldg(a.doff + root);
-    const int d = (int)(__ldg(a.doff + root + 1) - list_base);
-    if (task != cached) {
-      // stage the root's rows from the arena (L2-resident) into smem
-      const int wv = (d + 31) >> 5;
-      const uint32_t *src = a.bm + __ldg(a.bm_off + task);
-      for (int i = lane; i < d * wv; i += 32) {
-        const int r = i / wv, x = i - r * wv;
-        sm.adj[r * S + x] = __ldg(src + i);
-      }
-      cached = task;
-    }
-    {
-      // donated record: words 2..W+1 = C[s0], W+2..2W+1 = pending subset
-      const uint32_t cv = rec_word(rec, kRecHdr + lane);
-      const uint32_t pv = rec_word(rec, kRecHdr + W + lane);
-      if (lane < W) {
-        uint32_t cword, pword;
-        if (kind == 1) {
-          const int lo = lane * 32;
-          cword = d >= lo + 32 ? 0xffffffffu : (d > lo ? (1u << (d - lo)) - 1u : 0u);
-          pword = cword;
-        } else {
-          cword = cv;
-          pword = pv;
-        }
-        sm.C[s0][lane] = cword;
-        sm.P[s0][lane] = pword;
-      }
-    }
-    if (lane == 0) {
-      sm.below[s0] = 0;
-      sm.last[s0] = root;
-    }
-    __syncwarp();
-    tasks_done += (kind == 1);
-    if (s0 == k - 2) {
-      unsigned long long tot = 0;
-      acc += bulk_count<W, BYTES>(sm, s0, a, list_base, bytes, tot);
-      if (BYTES && lane == 0 && tot)
-        bytes += 4ull * (unsigned long long)(__ldg(a.doff + root + 1) - __ldg(a.doff + root));
-      continue;
-    }
-    int s = s0;
-    for (;;) {
-      // move_step: next unconsumed member at level s (lowest set bit)
-      const uint32_t pw = lane < W ? sm.P[s][lane] : 0u;
-      const unsigned nz = __ballot_sync(0xffffffffu, pw != 0u);
-      if (nz == 0u) {
-        if (BYTES && lane == 0) {
-          const unsigned long long b = sm.below[s];
-          if (b) {
-            const int32_t x = sm.last[s];
-            bytes += 4ull * (unsigned long long)(__ldg(a.doff + x + 1) - __ldg(a.doff + x));
-            if (s > s0) sm.below[s - 1] += b;
-          }
-        }
-        __syncwarp();
-        if (s == s0) break;
-        --s;
-        continue;
-      }
-      const int wl = __ffs(nz) - 1;
-      const uint32_t word = __shfl_sync(0xffffffffu, pw, wl);
-      const int i = wl * 32 + __ffs(word) - 1;
-      if (lane == wl) sm.P[s][wl] = word & (word - 1u);
-      // extend + lower + clique, fused: C_{s+1} = C_s & A[i]
-      uint32_t cw = 0u;
-      if (lane < W) {
-        cw = sm.C[s][lane] & sm.adj[i * S + lane];
-        sm.C[s + 1][lane] = cw;
-      }
-      const int cnt = __reduce_add_sync(0xffffffffu, __popc(cw));
-      __syncwarp();
-      ++nodes;
-      if (cnt >= k - s - 1) {
-        if (s + 1 == k - 2) {
-          unsigned long long tot = 0;
-          acc += bulk_count<W, BYTES>(sm, s + 1, a, list_base, bytes, tot);
-          if (BYTES && lane == 0 && tot) {
-            const int32_t x = __ldg(a.dnbr + list_base + i);
-            bytes += 4ull * (unsigned long long)(__ldg(a.doff + x + 1) - __ldg(a.doff + x));
-            sm.below[s] += tot;
-          }
-          __syncwarp();
-        } else {
-          ++s;
-          if (lane < W) sm.P[s][lane] = cw;
-          if (BYTES && lane == 0) {
-            sm.below[s] = 0;
-            sm.last[s] = __ldg(a.dnbr + list_base + i);
-          }
-          __syncwarp();
-        }
-      }
-      // on-device load balancing (opt mode): poll the idle-warp ring
-      if (!BYTES && a.lb_on && ++poll >= a.lb_poll) {
-        poll = 0;
-        ++polls;
-        if (donation_wanted(a.L, a.idle_min)) try_donate<W>(sm, a, s0, s, task);
-      }
+    const int64_t lb = __ldg(a.doff + root);
+    const int d = (int)(__ldg(a.doff + root + 1) - lb);
+    const bool stage = task != cached;
+    cached = task;
+    const int wv = (d + 31) >> 5;
+    if (WMAX <= 4) {
+      if (wv <= 1) run_task<1, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, tc);
+      else if (wv <= 2) run_task<(WMAX >= 2 ? 2 : 1), WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, tc);
+      else run_task<WMAX, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, tc);
+    } else {
+      run_task<WMAX, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, tc);
     }
   }
-  acc = warp_sum_u64(acc);
-  if (BYTES) bytes = warp_sum_u64(bytes);
+  const unsigned long long acc = warp_sum_u64(tc.acc);
+  const unsigned long long bytes = BYTES ? warp_sum_u64(tc.bytes) : 0;
   if (lane == 0) {
     atomicAdd(&a.counters[0], acc);
     if (BYTES) atomicAdd(&a.counters[1], bytes);
     atomicAdd(&a.counters[2], tasks_done);
-    atomicAdd(&a.counters[3], nodes);
-    atomicAdd(&a.counters[4], polls);
+    atomicAdd(&a.counters[3], tc.nodes);
+    atomicAdd(&a.counters[4], tc.polls);
   }
   warp_clock_end(a.L.lb, clk);
 }
@@ -512,32 +619,45 @@ static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask,
   return WM_OK;
 }
 
-template <int W, bool BYTES>
-static int launch_enum(Graph *g, const wm_cfg *cfg, CliqueArgs a, cudaStream_t s,
-                       int *warps_out) {
-  const size_t per_warp = sizeof(CliqueSmem<W>);
+struct EnumPlan {
+  int wpb = 0, blocks = 0, warps = 0;
+  size_t smem = 0;
+};
+
+template <int WMAX, bool BYTES>
+static int plan_enum(Graph *g, const wm_cfg *cfg, unsigned long long ntasks, bool lb_on,
+                     EnumPlan *p) {
+  const size_t per_warp = sizeof(CliqueSmem<WMAX>);
   int wpb = cfg->warps_per_block > 0 ? cfg->warps_per_block : 8;
   while (wpb > 1 && per_warp * wpb > 200 * 1024) wpb >>= 1;
   const size_t smem = per_warp * wpb;
-  auto kern = clique_enum_kernel<W, BYTES>;
+  auto kern = clique_enum_kernel<WMAX, BYTES>;
   WM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int bps = 0;
   WM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
   if (cfg->blocks_per_sm > 0 && cfg->blocks_per_sm < bps) bps = cfg->blocks_per_sm;
-  if (bps < 1) return fail(WM_ECAPACITY, "clique kernel W=%d does not fit on an SM", W);
+  if (bps < 1) return fail(WM_ECAPACITY, "clique kernel W=%d does not fit on an SM", WMAX);
   int blocks = g->num_sms * bps;
-  if (!a.lb_on) {  // no stealing: no point in more warps than tasks
-    const unsigned long long need = (a.ntasks + wpb - 1) / wpb;
+  if (!lb_on) {  // no stealing: no point in more warps than tasks
+    const unsigned long long need = (ntasks + wpb - 1) / wpb;
     if ((unsigned long long)blocks > need) blocks = (int)(need > 0 ? need : 1);
   }
-  const int warps = blocks * wpb;
-  int st = lb_prepare(g, a.L.lb, warps, (uint32_t)(kRecHdr + 2 * W), &a.L, s);
+  p->wpb = wpb;
+  p->blocks = blocks;
+  p->warps = blocks * wpb;
+  p->smem = smem;
+  return WM_OK;
+}
+
+template <int WMAX, bool BYTES>
+static int launch_enum(Graph *g, const wm_cfg *cfg, CliqueArgs a, const EnumPlan &p,
+                       cudaStream_t s) {
+  int st = lb_prepare(g, a.L.lb, p.warps, (uint32_t)(kRecHdr + 2 * WMAX), &a.L, s);
   if (st) return st;
-  a.idle_min = (int)((1.0 - cfg->lb_threshold) * warps);
+  a.idle_min = (int)((1.0 - cfg->lb_threshold) * p.warps);
   if (a.idle_min < 1) a.idle_min = 1;
-  kern<<<blocks, wpb * 32, smem, s>>>(a);
+  clique_enum_kernel<WMAX, BYTES><<<p.blocks, p.wpb * 32, p.smem, s>>>(a);
   WM_CUDA(cudaGetLastError());
-  *warps_out = warps;
   return WM_OK;
 }
 
@@ -571,11 +691,12 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   if (tmp_scan2 > tmp) tmp = tmp_scan2;
   if ((st = g->cub_tmp.ensure(tmp))) return st;
 
-  cudaEvent_t e0, e1, k0, k1;
+  cudaEvent_t e0, e1, k0, k1, kb;
   WM_CUDA(cudaEventCreate(&e0));
   WM_CUDA(cudaEventCreate(&e1));
   WM_CUDA(cudaEventCreate(&k0));
   WM_CUDA(cudaEventCreate(&k1));
+  WM_CUDA(cudaEventCreate(&kb));
   WM_CUDA(cudaEventRecord(e0, s));
   unsigned long long *ctr = g->counters.as<unsigned long long>();
   WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
@@ -629,27 +750,85 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
     res->launches += 1;
   }
   if ((st = g->arena.ensure(sizeof(uint32_t) * (arena_words + 1)))) return st;
+
+  // width classes, contiguous in the descending sort: 32, 16, 8, then <= 4
+  struct Cls { int wmax; unsigned long long begin, cnt; EnumPlan plan; };
+  Cls cls[4];
+  int ncls = 0;
+  {
+    unsigned long long begin = 0;
+    for (int c = 5; c >= 3; --c) {
+      if (hb[c]) cls[ncls++] = Cls{1 << c, begin, hb[c], EnumPlan()};
+      begin += hb[c];
+    }
+    const unsigned long long small = hb[0] + hb[1] + hb[2];
+    if (small) cls[ncls++] = Cls{4, begin, small, EnumPlan()};
+  }
+  // plan + allocate everything before the timed region
+  int max_warps = 0;
+  for (int i = 0; i < ncls; ++i) {
+    const unsigned long long cnt = cls[i].cnt;
+    const unsigned long long ro = (unsigned long long)cfg->shard_rank;
+    const unsigned long long nt = cnt > ro ? (cnt - ro + cfg->shard_count - 1) / cfg->shard_count : 0;
+    switch (cls[i].wmax) {
+#define WM_PLAN(WW)                                                                 \
+  case WW:                                                                          \
+    st = bytes ? plan_enum<WW, true>(g, cfg, nt, lb_on, &cls[i].plan)              \
+               : plan_enum<WW, false>(g, cfg, nt, lb_on, &cls[i].plan);            \
+    break;
+      WM_PLAN(4) WM_PLAN(8) WM_PLAN(16) WM_PLAN(32)
+#undef WM_PLAN
+    }
+    if (st) return st;
+    if (cls[i].plan.warps > max_warps) max_warps = cls[i].plan.warps;
+  }
+  {
+    uint32_t cap = 1;
+    while (cap < 8u * (uint32_t)max_warps) cap <<= 1;
+    if ((st = g->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap))) return st;
+  }
   LbState *lbs = g->lb.as<LbState>();
   int max_w = 0;
   double idle_w = 0, idle_tail_w = 0, tot_w = 0;
   int launched = 0;
   WM_CUDA(cudaEventRecord(k0, s));
-  // buckets are contiguous in the descending sort: W=32 first.  Build all
-  // bitmaps first, then enumerate.
+  // build all bitmaps, then enumerate
   for (int pass = 0; pass < 2; ++pass) {
+    if (pass == 1) WM_CUDA(cudaEventRecord(kb, s));
     unsigned long long begin = 0;
-    for (int c = 5; c >= 0; --c) {
+    for (int c = 5; c >= 0 && pass == 0; --c) {
       const unsigned long long cnt = hb[c];
       if (!cnt) continue;
-      const int W = 1 << c;
       CliqueArgs a;
       a.doff = g->dag_off.as<int64_t>();
       a.dnbr = g->dag_nbr.as<int32_t>();
       a.tasks = g->vals_out.as<int32_t>() + begin;
       a.bm_off = bm_off + begin;
       a.bm = g->arena.as<uint32_t>();
+      begin += cnt;
+      // every task of the bucket gets a bitmap so offsets stay shard-independent
+      switch (c) {
+#define WM_BCASE(CC, WW) \
+  case CC:               \
+    st = launch_build<WW>(g, a, cnt, s); \
+    break;
+        WM_BCASE(0, 1) WM_BCASE(1, 2) WM_BCASE(2, 4) WM_BCASE(3, 8) WM_BCASE(4, 16)
+        WM_BCASE(5, 32)
+#undef WM_BCASE
+      }
+      if (st) return st;
+      res->launches += 1;
+    }
+    for (int i = 0; i < ncls && pass == 1; ++i) {
+      CliqueArgs a;
+      a.doff = g->dag_off.as<int64_t>();
+      a.dnbr = g->dag_nbr.as<int32_t>();
+      a.tasks = g->vals_out.as<int32_t>() + cls[i].begin;
+      a.bm_off = bm_off + cls[i].begin;
+      a.bm = g->arena.as<uint32_t>();
       a.task_offset = (unsigned long long)cfg->shard_rank;
       a.task_stride = (unsigned long long)cfg->shard_count;
+      const unsigned long long cnt = cls[i].cnt;
       a.ntasks =
           cnt > a.task_offset ? (cnt - a.task_offset + a.task_stride - 1) / a.task_stride : 0;
       a.k = k;
@@ -658,37 +837,19 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
       a.idle_min = 1;
       a.L.lb = lbs + launched;
       a.counters = ctr;
-      begin += cnt;
       if (!a.ntasks) continue;
-      if (pass == 0) {
-        // only this shard's tasks need bitmaps, but building the bucket's
-        // full set keeps the offsets shard-independent; cheap next to the DFS
-        switch (c) {
-#define WM_BCASE(CC, WW) \
-  case CC:               \
-    st = launch_build<WW>(g, a, cnt, s); \
+      switch (cls[i].wmax) {
+#define WM_CASE(WW)                                                                  \
+  case WW:                                                                           \
+    st = bytes ? launch_enum<WW, true>(g, cfg, a, cls[i].plan, s)                    \
+               : launch_enum<WW, false>(g, cfg, a, cls[i].plan, s);                  \
     break;
-          WM_BCASE(0, 1) WM_BCASE(1, 2) WM_BCASE(2, 4) WM_BCASE(3, 8) WM_BCASE(4, 16)
-          WM_BCASE(5, 32)
-#undef WM_BCASE
-        }
-        if (st) return st;
-        res->launches += 1;
-        continue;
-      }
-      int warps = 0;
-      switch (c) {
-#define WM_CASE(CC, WW)                                                      \
-  case CC:                                                                   \
-    st = bytes ? launch_enum<WW, true>(g, cfg, a, s, &warps)                 \
-               : launch_enum<WW, false>(g, cfg, a, s, &warps);               \
-    break;
-        WM_CASE(0, 1) WM_CASE(1, 2) WM_CASE(2, 4) WM_CASE(3, 8) WM_CASE(4, 16) WM_CASE(5, 32)
+        WM_CASE(4) WM_CASE(8) WM_CASE(16) WM_CASE(32)
 #undef WM_CASE
       }
       if (st) return st;
-      if (W > max_w) max_w = W;
-      if (warps > res->warps) res->warps = warps;
+      if (cls[i].wmax > max_w) max_w = cls[i].wmax;
+      if (cls[i].plan.warps > res->warps) res->warps = cls[i].plan.warps;
       res->launches += 2;
       ++launched;
     }
@@ -701,13 +862,18 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
     WM_CUDA(cudaMemcpyAsync(hl, lbs, sizeof(LbState) * launched, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaEventRecord(e1, s));
   WM_CUDA(cudaStreamSynchronize(s));
-  float kms = 0, dms = 0;
-  WM_CUDA(cudaEventElapsedTime(&kms, k0, k1));
+  float kms = 0, dms = 0, bms = 0;
+  WM_CUDA(cudaEventElapsedTime(&bms, k0, kb));
+  WM_CUDA(cudaEventElapsedTime(&kms, kb, k1));
   WM_CUDA(cudaEventElapsedTime(&dms, e0, e1));
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   cudaEventDestroy(k0);
   cudaEventDestroy(k1);
+  cudaEventDestroy(kb);
+  res->build_ms = bms;
+  res->d2h_bytes = sizeof hb + (ntask ? sizeof arena_words : 0) + sizeof hc +
+                   sizeof(LbState) * (uint64_t)launched;
   res->clique_count = hc[0];
   res->leaves = hc[0];
   res->alg_bytes = bytes ? hc[1] : 0;

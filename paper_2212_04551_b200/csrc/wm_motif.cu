@@ -567,6 +567,9 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   cudaEventDestroy(e1);
   cudaEventDestroy(k0);
   cudaEventDestroy(k1);
+  res->h2d_bytes = sizeof(uint32_t) * app->dict_len;
+  res->d2h_bytes = sizeof ntask + sizeof hc + sizeof(unsigned long long) * app->pattern_count +
+                   sizeof hl;
   res->leaves = hc[0];
   res->alg_bytes = bytes ? hc[1] : 0;
   res->tasks = hc[2];

@@ -279,7 +279,8 @@ def run(g: CsrGraph, app: Application, *, mode: str = "wc", warps: int = None,
         idle_warp_fraction_tail=res.idle_warp_fraction_tail, tasks=int(res.tasks),
         launches=int(res.launches), devices=shard[1], order=order,
         extra={"bucket_words": res.bucket_words, "nodes": int(res.nodes),
-               "polls": int(res.polls)})
+               "polls": int(res.polls), "build_ms": res.build_ms,
+               "h2d_bytes": int(res.h2d_bytes), "d2h_bytes": int(res.d2h_bytes)})
     if reduce and shard[1] > 1:
         from . import parallel
         out = parallel.allreduce_result(out)
