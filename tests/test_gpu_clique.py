@@ -92,8 +92,14 @@ def test_cfg3_scale_counts(scale_golden, cuda):
             kw = {"balance_config": BalanceConfig(threshold=1.0)} if mode == "opt" else {}
             r = run_clique(g, k, mode=mode, **kw)
             assert r.clique_count == want["count"], (k, mode, r.clique_count, want["count"])
-    r = run_clique(g, 6, count_bytes=True)
-    assert r.alg_bytes == scale_golden["cfg3"]["clique"]["6"]["alg_bytes_degree_order"]
+    for k in range(9, 13):
+        want = scale_golden["cfg3"]["clique"].get(str(k))
+        if want:
+            r = run_clique(g, k, mode="opt", balance_config=BalanceConfig(threshold=1.0))
+            assert r.clique_count == want["count"], (k, r.clique_count, want["count"])
+    for k in (5, 6):
+        r = run_clique(g, k, count_bytes=True)
+        assert r.alg_bytes == scale_golden["cfg3"]["clique"][str(k)]["alg_bytes_degree_order"]
 
 
 def test_sharded_runs_sum_to_total(cuda):
