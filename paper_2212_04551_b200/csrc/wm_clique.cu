@@ -232,8 +232,8 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
 
 template <int WMAX> struct CliqueSmem {
   static constexpr int D = 32 * WMAX;
-  static constexpr int S = (WMAX == 1) ? 1 : WMAX + 1;
-  uint32_t adj[D * S];                 // local DAG rows, stride w+1 (odd) for width w
+  static constexpr int S = WMAX;
+  uint32_t adj[D * S];                 // local DAG rows, stride w (16B-aligned vector loads)
   uint32_t C[kMaxK * WMAX];            // candidate set per level  [s * w + x]
   uint32_t P[kMaxK * WMAX];            // unconsumed members       [s * w + x]
   unsigned long long below[kMaxK];     // leaves under the level's node (B_alg)
@@ -258,8 +258,25 @@ struct CliqueArgs {
 };
 
 template <int w> struct Width {
-  static constexpr int S = (w == 1) ? 1 : w + 1;
+  static constexpr int S = w;
 };
+
+// one local-DAG row into registers with 64/128-bit shared loads
+template <int w>
+__device__ __forceinline__ void load_row(const uint32_t *p, uint32_t (&r)[w]) {
+  if constexpr (w % 4 == 0) {
+#pragma unroll
+    for (int q = 0; q < w / 4; ++q) {
+      const uint4 v = reinterpret_cast<const uint4 *>(p)[q];
+      r[4 * q] = v.x; r[4 * q + 1] = v.y; r[4 * q + 2] = v.z; r[4 * q + 3] = v.w;
+    }
+  } else if constexpr (w == 2) {
+    const uint2 v = *reinterpret_cast<const uint2 *>(p);
+    r[0] = v.x; r[1] = v.y;
+  } else {
+    r[0] = p[0];
+  }
+}
 
 __device__ __forceinline__ unsigned long long outdeg_bytes(const CliqueArgs &a, int32_t u) {
   return 4ull * (unsigned long long)(__ldg(a.doff + u + 1) - __ldg(a.doff + u));
@@ -281,7 +298,8 @@ __device__ __forceinline__ unsigned long long bulk2(const uint32_t *adj, const u
     if (c[q] == 0u) continue;
     if ((c[q] >> lane) & 1u) {
       const int j = q * 32 + lane;
-      const uint32_t *row = adj + j * S;
+      uint32_t row[w];
+      load_row<w>(adj + j * S, row);
       uint32_t t = 0;
 #pragma unroll
       for (int x = 0; x < w; ++x) t += __popc(c[x] & row[x]);
@@ -313,7 +331,8 @@ __device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const u
     if (jw == 0u) continue;
     if ((jw >> lane) & 1u) {
       const int j = q * 32 + lane;
-      const uint32_t *rj = adj + j * S;
+      uint32_t rj[w];
+      load_row<w>(adj + j * S, rj);
       uint32_t cj[w];
       int cnt = 0;
 #pragma unroll
@@ -329,7 +348,8 @@ __device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const u
           while (m) {
             const int l = y * 32 + __ffs(m) - 1;
             m &= m - 1u;
-            const uint32_t *rl = adj + l * S;
+            uint32_t rl[w];
+            load_row<w>(adj + l * S, rl);
             uint32_t t = 0;
 #pragma unroll
             for (int x = 0; x < w; ++x) t += __popc(cj[x] & rl[x]);
