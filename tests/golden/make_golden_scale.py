@@ -79,6 +79,24 @@ def main():
                           "cpu_s": round(time.time() - t, 2)}
             print("%s motif k=%d leaves=%d %.1fs" % (name, k, r["leaves"], time.time() - t), flush=True)
             json.dump(out, open(OUT, "w"), indent=1)
+    # cfg4 (R-MAT s20 ef16, Graph500 skew, permuted ids): root suffixes
+    # [n - s, n) == the induced subgraph on the last s ids
+    g4 = synth.config_graph("cfg4")
+    r4 = out.setdefault("cfg4", {})
+    r4.update({"digest": digest(g4), "n": g4.n, "m": g4.m, "max_degree": g4.max_degree,
+               "recipe": "rmat(20, 16, a=.57, b=.19, c=.19, seed=1), ids permuted (seed 20)"})
+    suf = r4.setdefault("motif_suffix", {})
+    for k, s in ((5, 16384), (6, 4096), (5, 4096), (7, 2048)):
+        key = "k%d_s%d" % (k, s)
+        if key in suf:
+            continue
+        d = canon.build_dictionary(k)
+        t = time.time()
+        r = oracle.motif_run(g4, k, d.table, d.pattern_count, root_begin=g4.n - s, root_end=g4.n)
+        suf[key] = {"k": k, "suffix": s, "hist": r["hist"], "leaves": r["leaves"],
+                    "cpu_s": round(time.time() - t, 2), "oracle": "wmo_motif_run"}
+        print("cfg4 motif %s leaves=%d %.1fs" % (key, r["leaves"], time.time() - t), flush=True)
+        json.dump(out, open(OUT, "w"), indent=1)
     json.dump(out, open(OUT, "w"), indent=1)
 
 

@@ -82,6 +82,25 @@ def test_cfg_scale_histograms(scale_golden, cuda):
                 assert r.pattern_counts == want["hist"], (name, k, mode)
 
 
+def test_cfg4_rmat_root_suffix(scale_golden, cuda):
+    """Config 4 (skewed R-MAT s20): bounded root-suffix runs vs the pinned
+    restatement; the suffix is exactly the induced subgraph on the last ids."""
+    import hashlib
+    import numpy as np
+    from paper_2212_04551_b200 import BalanceConfig, run_motifs, synth
+    g = synth.config_graph("cfg4")
+    h = hashlib.sha256()
+    h.update(np.asarray(g.offsets, dtype="<i8").tobytes())
+    h.update(np.asarray(g.neighbors_array, dtype="<i4").tobytes())
+    assert h.hexdigest() == scale_golden["cfg4"]["digest"]
+    for key, want in scale_golden["cfg4"]["motif_suffix"].items():
+        k, s = want["k"], want["suffix"]
+        for mode in ("wc", "opt"):
+            kw = {"balance_config": BalanceConfig(threshold=1.0)} if mode == "opt" else {}
+            r = run_motifs(g, k, dictionary(k), mode=mode, roots=(g.n - s, g.n), **kw)
+            assert r.pattern_counts == want["hist"], (key, mode)
+
+
 def test_root_suffix_and_shards(cuda):
     """Root suffix == induced suffix graph; cyclic shards sum to the total."""
     from paper_2212_04551_b200 import gnp_random_graph, run_motifs
