@@ -8,6 +8,7 @@
 // no CPU fallback.
 #include <cstdarg>
 #include <cstring>
+#include <mutex>
 #include <string>
 
 #include "wm_common.cuh"
@@ -68,9 +69,9 @@ int lb_prepare(Graph *g, LbState *lb, int warps, uint32_t words, LbShared *out, 
   uint32_t cap = 1;
   while (cap < 8u * (uint32_t)warps) cap <<= 1;
   int st;
-  if ((st = g->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap))) return st;
+  if ((st = g->ws->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap))) return st;
   out->lb = lb;
-  out->ring = g->ring.as<uint32_t>();
+  out->ring = g->ws->ring.as<uint32_t>();
   out->cap = cap;
   out->words = words;
   lb_init_kernel<<<(int)((cap + 255) / 256), 256, 0, s>>>(lb, warps, out->ring, cap);
@@ -101,6 +102,35 @@ void finish_lb_stats(const LbState &h, wm_result *res) {
   res->peak_ext = h.peak_ext;
 }
 
+static std::mutex g_ws_mu;
+static Workspace *g_ws[64];
+
+int workspace_get(Workspace **out) {
+  int dev = 0;
+  WM_CUDA(cudaGetDevice(&dev));
+  if (dev < 0 || dev >= 64) return fail(WM_EINVAL, "device %d out of range", dev);
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  if (!g_ws[dev]) {
+    Workspace *w = new Workspace();
+    w->device = dev;
+    cudaError_t e = cudaDeviceGetAttribute(&w->num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->own_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaDeviceGetDefaultMemPool(&w->pool, dev);
+    if (e == cudaSuccess) {
+      uint64_t thr = ~0ull;
+      e = cudaMemPoolSetAttribute(w->pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    for (int i = 0; i < 6 && e == cudaSuccess; ++i) e = cudaEventCreate(&w->ev[i]);
+    if (e != cudaSuccess) {
+      delete w;
+      return fail(WM_ECUDA, "workspace init failed: %s", cudaGetErrorString(e));
+    }
+    g_ws[dev] = w;
+  }
+  *out = g_ws[dev];
+  return WM_OK;
+}
+
 }  // namespace wm
 
 using namespace wm;
@@ -112,10 +142,23 @@ int wm_abi_version(void) { return WM_ABI_VERSION; }
 const char *wm_last_error(void) { return g_last_error.c_str(); }
 
 static int graph_init(Graph *g) {
-  WM_CUDA(cudaGetDevice(&g->device));
-  WM_CUDA(cudaDeviceGetAttribute(&g->num_sms, cudaDevAttrMultiProcessorCount, g->device));
-  WM_CUDA(cudaStreamCreateWithFlags(&g->own_stream, cudaStreamNonBlocking));
+  int st = workspace_get(&g->ws);
+  if (st) return st;
+  g->device = g->ws->device;
+  g->num_sms = g->ws->num_sms;
   return WM_OK;
+}
+
+// graph arrays come from the device's stream-ordered pool (release threshold
+// = unlimited), so create/destroy cycles reuse memory without device syncs
+static cudaError_t graph_alloc(Graph *g) {
+  cudaStream_t s = g->ws->own_stream;
+  cudaError_t e = cudaMallocFromPoolAsync(reinterpret_cast<void **>(&g->offsets),
+                                          sizeof(int64_t) * (g->n + 1), g->ws->pool, s);
+  if (e == cudaSuccess)
+    e = cudaMallocFromPoolAsync(reinterpret_cast<void **>(&g->neighbors),
+                                sizeof(int32_t) * (g->nnz > 0 ? g->nnz : 1), g->ws->pool, s);
+  return e;
 }
 
 int wm_graph_create(const wm_csr *csr, void **out) {
@@ -129,27 +172,27 @@ int wm_graph_create(const wm_csr *csr, void **out) {
     return fail(WM_EINVAL, "null CSR arrays");
   if (csr->offsets[0] != 0 || csr->offsets[csr->n] != csr->nnz)
     return fail(WM_EINVAL, "offsets do not span nnz=%lld", (long long)csr->nnz);
+  int64_t md = 0;
+  for (int64_t v = 0; v < csr->n; ++v) {
+    int64_t d = csr->offsets[v + 1] - csr->offsets[v];
+    if (d < 0) return fail(WM_EINVAL, "offsets decrease at vertex %lld", (long long)v);
+    if (d > md) md = d;
+  }
   Graph *g = new Graph();
   int st = graph_init(g);
   if (st) { delete g; return st; }
   g->n = csr->n;
   g->nnz = csr->nnz;
-  int64_t md = 0;
-  for (int64_t v = 0; v < csr->n; ++v) {
-    int64_t d = csr->offsets[v + 1] - csr->offsets[v];
-    if (d < 0) { delete g; return fail(WM_EINVAL, "offsets decrease at vertex %lld", (long long)v); }
-    if (d > md) md = d;
-  }
   g->max_degree = md;
-  cudaError_t e = cudaMalloc(&g->offsets, sizeof(int64_t) * (g->n + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&g->neighbors, sizeof(int32_t) * (g->nnz > 0 ? g->nnz : 1));
+  cudaStream_t s = g->ws->own_stream;
+  cudaError_t e = graph_alloc(g);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(g->offsets, csr->offsets, sizeof(int64_t) * (g->n + 1),
-                        cudaMemcpyHostToDevice, g->own_stream);
+                        cudaMemcpyHostToDevice, s);
   if (e == cudaSuccess && g->nnz > 0)
     e = cudaMemcpyAsync(g->neighbors, csr->neighbors, sizeof(int32_t) * g->nnz,
-                        cudaMemcpyHostToDevice, g->own_stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(g->own_stream);
+                        cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     wm_graph_destroy(g);
     return fail(WM_ECUDA, "graph upload failed: %s", cudaGetErrorString(e));
@@ -158,35 +201,58 @@ int wm_graph_create(const wm_csr *csr, void **out) {
   return WM_OK;
 }
 
+__global__ void max_degree_kernel(int64_t n, const int64_t *__restrict__ off,
+                                  unsigned long long *__restrict__ out) {
+  unsigned long long m = 0;
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
+    m = d > m ? d : m;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
+    m = y > m ? y : m;
+  }
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
 int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
                            const int32_t *d_neighbors, void **out) {
   g_last_error.clear();
   if (!out || !d_offsets || n < 1) return fail(WM_EINVAL, "bad device graph arguments");
+  if (n >= (1ll << 31) - 1) return fail(WM_EINVAL, "n=%lld exceeds int32 vertex ids",
+                                        (long long)n);
   Graph *g = new Graph();
   int st = graph_init(g);
   if (st) { delete g; return st; }
   g->n = n;
   g->nnz = nnz;
-  cudaError_t e = cudaMalloc(&g->offsets, sizeof(int64_t) * (n + 1));
-  if (e == cudaSuccess) e = cudaMalloc(&g->neighbors, sizeof(int32_t) * (nnz > 0 ? nnz : 1));
+  cudaStream_t s = g->ws->own_stream;
+  cudaError_t e = graph_alloc(g);
   if (e == cudaSuccess)
     e = cudaMemcpyAsync(g->offsets, d_offsets, sizeof(int64_t) * (n + 1),
-                        cudaMemcpyDeviceToDevice, g->own_stream);
+                        cudaMemcpyDeviceToDevice, s);
   if (e == cudaSuccess && nnz > 0)
     e = cudaMemcpyAsync(g->neighbors, d_neighbors, sizeof(int32_t) * nnz,
-                        cudaMemcpyDeviceToDevice, g->own_stream);
-  // max degree for capacity planning
-  int64_t *h_off = nullptr;
-  if (e == cudaSuccess) e = cudaMallocHost(&h_off, sizeof(int64_t) * (n + 1));
-  if (e == cudaSuccess)
-    e = cudaMemcpyAsync(h_off, d_offsets, sizeof(int64_t) * (n + 1), cudaMemcpyDeviceToHost,
-                        g->own_stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(g->own_stream);
+                        cudaMemcpyDeviceToDevice, s);
+  // max degree for capacity planning, reduced on the device
   if (e == cudaSuccess) {
-    for (int64_t v = 0; v < n; ++v)
-      if (h_off[v + 1] - h_off[v] > g->max_degree) g->max_degree = h_off[v + 1] - h_off[v];
+    const int r = g->ws->counters.ensure(sizeof(unsigned long long) * 64);
+    if (r) { wm_graph_destroy(g); return r; }
+    unsigned long long *md = g->ws->counters.as<unsigned long long>();
+    e = cudaMemsetAsync(md, 0, sizeof(unsigned long long), s);
+    if (e == cudaSuccess) {
+      const int64_t blocks = (n + 255) / 256 < (int64_t)g->num_sms * 8 ? (n + 255) / 256
+                                                                      : (int64_t)g->num_sms * 8;
+      max_degree_kernel<<<(int)blocks, 256, 0, s>>>(n, g->offsets, md);
+      e = cudaGetLastError();
+    }
+    unsigned long long h = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, md, sizeof h, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    g->max_degree = (int64_t)h;
   }
-  if (h_off) cudaFreeHost(h_off);
   if (e != cudaSuccess) {
     wm_graph_destroy(g);
     return fail(WM_ECUDA, "device graph copy failed: %s", cudaGetErrorString(e));
@@ -198,9 +264,11 @@ int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
 void wm_graph_destroy(void *gp) {
   Graph *g = static_cast<Graph *>(gp);
   if (!g) return;
-  if (g->offsets) cudaFree(g->offsets);
-  if (g->neighbors) cudaFree(g->neighbors);
-  if (g->own_stream) cudaStreamDestroy(g->own_stream);
+  if (g->ws) {
+    cudaStream_t s = g->ws->own_stream;
+    if (g->offsets) cudaFreeAsync(g->offsets, s);
+    if (g->neighbors) cudaFreeAsync(g->neighbors, s);
+  }
   delete g;
 }
 
@@ -227,7 +295,7 @@ int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
   uint64_t *user_hist = res->pattern_counts;
   memset(res, 0, sizeof *res);
   res->pattern_counts = user_hist;
-  cudaStream_t s = cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : g->own_stream;
+  cudaStream_t s = cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : g->ws->own_stream;
   int dev = 0;
   WM_CUDA(cudaGetDevice(&dev));
   if (dev != g->device)

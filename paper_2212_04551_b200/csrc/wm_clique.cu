@@ -688,62 +688,57 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   const bool bytes = cfg->count_bytes != 0;
   const bool lb_on = cfg->mode == WM_MODE_OPT && !bytes;
   int st;
-  if ((st = g->dag_off.ensure(sizeof(int64_t) * (n + 1)))) return st;
-  if ((st = g->outdeg.ensure(sizeof(int32_t) * (n + 1)))) return st;
-  if ((st = g->dag_nbr.ensure(sizeof(int32_t) * (g->nnz / 2 + 1)))) return st;
-  if ((st = g->keys_in.ensure(sizeof(uint32_t) * n))) return st;
-  if ((st = g->keys_out.ensure(sizeof(uint32_t) * n))) return st;
-  if ((st = g->vals_in.ensure(sizeof(int32_t) * n))) return st;
-  if ((st = g->vals_out.ensure(sizeof(int32_t) * n))) return st;
-  if ((st = g->hist.ensure(sizeof(unsigned long long) * (n + 1)))) return st;  // task words
-  if ((st = g->table.ensure(sizeof(unsigned long long) * (n + 1)))) return st; // bm_off
-  if ((st = g->counters.ensure(sizeof(unsigned long long) * 64))) return st;
-  if ((st = g->lb.ensure(sizeof(LbState) * 8))) return st;
+  if ((st = g->ws->dag_off.ensure(sizeof(int64_t) * (n + 1)))) return st;
+  if ((st = g->ws->outdeg.ensure(sizeof(int32_t) * (n + 1)))) return st;
+  if ((st = g->ws->dag_nbr.ensure(sizeof(int32_t) * (g->nnz / 2 + 1)))) return st;
+  if ((st = g->ws->keys_in.ensure(sizeof(uint32_t) * n))) return st;
+  if ((st = g->ws->keys_out.ensure(sizeof(uint32_t) * n))) return st;
+  if ((st = g->ws->vals_in.ensure(sizeof(int32_t) * n))) return st;
+  if ((st = g->ws->vals_out.ensure(sizeof(int32_t) * n))) return st;
+  if ((st = g->ws->hist.ensure(sizeof(unsigned long long) * (n + 1)))) return st;  // task words
+  if ((st = g->ws->table.ensure(sizeof(unsigned long long) * (n + 1)))) return st; // bm_off
+  if ((st = g->ws->counters.ensure(sizeof(unsigned long long) * 64))) return st;
+  if ((st = g->ws->lb.ensure(sizeof(LbState) * 8))) return st;
   size_t tmp_scan = 0, tmp_sort = 0, tmp_scan2 = 0;
-  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, g->outdeg.as<int32_t>(),
-                                        g->dag_off.as<int64_t>(), (int)(n + 1), s));
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, g->ws->outdeg.as<int32_t>(),
+                                        g->ws->dag_off.as<int64_t>(), (int)(n + 1), s));
   WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
-      nullptr, tmp_sort, g->keys_in.as<uint32_t>(), g->keys_out.as<uint32_t>(),
-      g->vals_in.as<int32_t>(), g->vals_out.as<int32_t>(), (int)n, 0, 32, s));
-  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan2, g->hist.as<unsigned long long>(),
-                                        g->table.as<unsigned long long>(), (int)(n + 1), s));
+      nullptr, tmp_sort, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
+      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0, 32, s));
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan2, g->ws->hist.as<unsigned long long>(),
+                                        g->ws->table.as<unsigned long long>(), (int)(n + 1), s));
   size_t tmp = tmp_scan > tmp_sort ? tmp_scan : tmp_sort;
   if (tmp_scan2 > tmp) tmp = tmp_scan2;
-  if ((st = g->cub_tmp.ensure(tmp))) return st;
+  if ((st = g->ws->cub_tmp.ensure(tmp))) return st;
 
-  cudaEvent_t e0, e1, k0, k1, kb;
-  WM_CUDA(cudaEventCreate(&e0));
-  WM_CUDA(cudaEventCreate(&e1));
-  WM_CUDA(cudaEventCreate(&k0));
-  WM_CUDA(cudaEventCreate(&k1));
-  WM_CUDA(cudaEventCreate(&kb));
+  cudaEvent_t e0 = g->ws->ev[0], e1 = g->ws->ev[1], k0 = g->ws->ev[2], k1 = g->ws->ev[3], kb = g->ws->ev[4];
   WM_CUDA(cudaEventRecord(e0, s));
-  unsigned long long *ctr = g->counters.as<unsigned long long>();
+  unsigned long long *ctr = g->ws->counters.as<unsigned long long>();
   WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
   const int tpb = 256;
   const int vblocks = (int)((n * 32 + tpb - 1) / tpb < (int64_t)g->num_sms * 64
                                 ? (n * 32 + tpb - 1) / tpb
                                 : (int64_t)g->num_sms * 64);
   orient_count_kernel<<<vblocks, tpb, 0, s>>>(n, g->offsets, g->neighbors, order,
-                                              g->outdeg.as<int32_t>());
-  WM_CUDA(cudaMemsetAsync(g->outdeg.as<int32_t>() + n, 0, sizeof(int32_t), s));
-  size_t tb = g->cub_tmp.bytes;
-  WM_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.ptr, tb, g->outdeg.as<int32_t>(),
-                                        g->dag_off.as<int64_t>(), (int)(n + 1), s));
+                                              g->ws->outdeg.as<int32_t>());
+  WM_CUDA(cudaMemsetAsync(g->ws->outdeg.as<int32_t>() + n, 0, sizeof(int32_t), s));
+  size_t tb = g->ws->cub_tmp.bytes;
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, g->ws->outdeg.as<int32_t>(),
+                                        g->ws->dag_off.as<int64_t>(), (int)(n + 1), s));
   orient_fill_kernel<<<vblocks, tpb, 0, s>>>(n, g->offsets, g->neighbors, order,
-                                             g->dag_off.as<int64_t>(), g->dag_nbr.as<int32_t>());
+                                             g->ws->dag_off.as<int64_t>(), g->ws->dag_nbr.as<int32_t>());
   const int64_t rb = cfg->root_begin < 0 ? 0 : cfg->root_begin;
   const int64_t re = (cfg->root_end < 0 || cfg->root_end > n) ? n : cfg->root_end;
   const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
                                 ? (n + tpb - 1) / tpb
                                 : (int64_t)g->num_sms * 16);
-  task_keys_kernel<<<eblocks, tpb, 0, s>>>(n, g->outdeg.as<int32_t>(), k, rb, re,
-                                           g->keys_in.as<uint32_t>(), g->vals_in.as<int32_t>());
-  tb = g->cub_tmp.bytes;
+  task_keys_kernel<<<eblocks, tpb, 0, s>>>(n, g->ws->outdeg.as<int32_t>(), k, rb, re,
+                                           g->ws->keys_in.as<uint32_t>(), g->ws->vals_in.as<int32_t>());
+  tb = g->ws->cub_tmp.bytes;
   WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
-      g->cub_tmp.ptr, tb, g->keys_in.as<uint32_t>(), g->keys_out.as<uint32_t>(),
-      g->vals_in.as<int32_t>(), g->vals_out.as<int32_t>(), (int)n, 0, 32, s));
-  bucket_count_kernel<<<eblocks, tpb, 0, s>>>(n, g->keys_out.as<uint32_t>(), ctr + 8);
+      g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
+      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0, 32, s));
+  bucket_count_kernel<<<eblocks, tpb, 0, s>>>(n, g->ws->keys_out.as<uint32_t>(), ctr + 8);
   unsigned long long hb[8];
   WM_CUDA(cudaMemcpyAsync(hb, ctr + 8, sizeof hb, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
@@ -756,20 +751,20 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   unsigned long long ntask = 0;
   for (int c = 0; c < 6; ++c) ntask += hb[c];
   // bitmap arena offsets: exclusive scan of d * ceil(d/32) over the sorted tasks
-  unsigned long long *words = g->hist.as<unsigned long long>();
-  unsigned long long *bm_off = g->table.as<unsigned long long>();
+  unsigned long long *words = g->ws->hist.as<unsigned long long>();
+  unsigned long long *bm_off = g->ws->table.as<unsigned long long>();
   unsigned long long arena_words = 0;
   if (ntask) {
-    task_words_kernel<<<eblocks, tpb, 0, s>>>(ntask, g->keys_out.as<uint32_t>(), words);
+    task_words_kernel<<<eblocks, tpb, 0, s>>>(ntask, g->ws->keys_out.as<uint32_t>(), words);
     WM_CUDA(cudaMemsetAsync(words + ntask, 0, sizeof(unsigned long long), s));
-    tb = g->cub_tmp.bytes;
-    WM_CUDA(cub::DeviceScan::ExclusiveSum(g->cub_tmp.ptr, tb, words, bm_off, (int)(ntask + 1), s));
+    tb = g->ws->cub_tmp.bytes;
+    WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, words, bm_off, (int)(ntask + 1), s));
     WM_CUDA(cudaMemcpyAsync(&arena_words, bm_off + ntask, sizeof arena_words,
                             cudaMemcpyDeviceToHost, s));
     WM_CUDA(cudaStreamSynchronize(s));
     res->launches += 1;
   }
-  if ((st = g->arena.ensure(sizeof(uint32_t) * (arena_words + 1)))) return st;
+  if ((st = g->ws->arena.ensure(sizeof(uint32_t) * (arena_words + 1)))) return st;
 
   // width classes, contiguous in the descending sort: 32, 16, 8, then <= 4
   struct Cls { int wmax; unsigned long long begin, cnt; EnumPlan plan; };
@@ -805,9 +800,9 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   {
     uint32_t cap = 1;
     while (cap < 8u * (uint32_t)max_warps) cap <<= 1;
-    if ((st = g->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap))) return st;
+    if ((st = g->ws->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap))) return st;
   }
-  LbState *lbs = g->lb.as<LbState>();
+  LbState *lbs = g->ws->lb.as<LbState>();
   int max_w = 0;
   double idle_w = 0, idle_tail_w = 0, tot_w = 0;
   int launched = 0;
@@ -820,11 +815,11 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
       const unsigned long long cnt = hb[c];
       if (!cnt) continue;
       CliqueArgs a;
-      a.doff = g->dag_off.as<int64_t>();
-      a.dnbr = g->dag_nbr.as<int32_t>();
-      a.tasks = g->vals_out.as<int32_t>() + begin;
+      a.doff = g->ws->dag_off.as<int64_t>();
+      a.dnbr = g->ws->dag_nbr.as<int32_t>();
+      a.tasks = g->ws->vals_out.as<int32_t>() + begin;
       a.bm_off = bm_off + begin;
-      a.bm = g->arena.as<uint32_t>();
+      a.bm = g->ws->arena.as<uint32_t>();
       begin += cnt;
       // every task of the bucket gets a bitmap so offsets stay shard-independent
       switch (c) {
@@ -841,11 +836,11 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
     }
     for (int i = 0; i < ncls && pass == 1; ++i) {
       CliqueArgs a;
-      a.doff = g->dag_off.as<int64_t>();
-      a.dnbr = g->dag_nbr.as<int32_t>();
-      a.tasks = g->vals_out.as<int32_t>() + cls[i].begin;
+      a.doff = g->ws->dag_off.as<int64_t>();
+      a.dnbr = g->ws->dag_nbr.as<int32_t>();
+      a.tasks = g->ws->vals_out.as<int32_t>() + cls[i].begin;
       a.bm_off = bm_off + cls[i].begin;
-      a.bm = g->arena.as<uint32_t>();
+      a.bm = g->ws->arena.as<uint32_t>();
       a.task_offset = (unsigned long long)cfg->shard_rank;
       a.task_stride = (unsigned long long)cfg->shard_count;
       const unsigned long long cnt = cls[i].cnt;
@@ -886,11 +881,6 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   WM_CUDA(cudaEventElapsedTime(&bms, k0, kb));
   WM_CUDA(cudaEventElapsedTime(&kms, kb, k1));
   WM_CUDA(cudaEventElapsedTime(&dms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(k0);
-  cudaEventDestroy(k1);
-  cudaEventDestroy(kb);
   res->build_ms = bms;
   res->d2h_bytes = sizeof hb + (ntask ? sizeof arena_words : 0) + sizeof hc +
                    sizeof(LbState) * (uint64_t)launched;

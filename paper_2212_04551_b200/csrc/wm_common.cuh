@@ -289,6 +289,23 @@ struct DeviceBuffer {
   template <typename T> T *as() const { return static_cast<T *>(ptr); }
 };
 
+// Per-device scratch, shared by every graph handle on that device: grow-only
+// buffers reused across runs and across graphs, so a fresh upload (the e2e
+// path) pays no cudaMalloc/cudaFree.  Calls are not re-entrant per device
+// (header contract); `mu` serialises concurrent callers.
+struct Workspace {
+  int device = 0;
+  int num_sms = 0;
+  cudaStream_t own_stream = nullptr;
+  cudaMemPool_t pool = nullptr;  // stream-ordered pool for graph arrays
+  DeviceBuffer dag_off, dag_nbr, outdeg, keys_in, keys_out, vals_in, vals_out, cub_tmp;
+  DeviceBuffer lb, ring, counters, hist, arena, table, listing;
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+// returns the workspace of the current device (created on first use)
+int workspace_get(Workspace **out);
+
 struct Graph {
   int64_t n = 0, nnz = 0;
   int64_t max_degree = 0;
@@ -296,10 +313,7 @@ struct Graph {
   int num_sms = 0;
   int64_t *offsets = nullptr;   // device [n+1]
   int32_t *neighbors = nullptr; // device [nnz]
-  cudaStream_t own_stream = nullptr;
-  // scratch (grow-only, reused across runs)
-  DeviceBuffer dag_off, dag_nbr, outdeg, keys_in, keys_out, vals_in, vals_out, cub_tmp;
-  DeviceBuffer lb, ring, counters, hist, arena, table, pub;
+  Workspace *ws = nullptr;
 };
 
 // Allocates the balancer's ring for `warps` and initialises lb (one

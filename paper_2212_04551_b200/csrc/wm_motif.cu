@@ -450,21 +450,21 @@ static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s
   const unsigned long long per_warp = a.warp_stride * sizeof(uint32_t);
   size_t free_b = 0, total_b = 0;
   WM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const unsigned long long budget = (unsigned long long)(free_b * 0.6) + g->arena.bytes;
+  const unsigned long long budget = (unsigned long long)(free_b * 0.6) + g->ws->arena.bytes;
   while (blocks > 1 && (unsigned long long)blocks * wpb * per_warp > budget) blocks >>= 1;
   if (!a.lb_on) {
     const unsigned long long need = (a.ntasks + wpb - 1) / wpb;
     if ((unsigned long long)blocks > need) blocks = (long long)(need > 0 ? need : 1);
   }
   const int warps = (int)blocks * wpb;
-  int st = g->arena.ensure((size_t)per_warp * warps);
+  int st = g->ws->arena.ensure((size_t)per_warp * warps);
   if (st) return st;
   if (!launch) {  // allocation pass, outside the timed region
     uint32_t cap = 1;
     while (cap < 8u * (uint32_t)warps) cap <<= 1;
-    return g->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap);
+    return g->ws->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap);
   }
-  a.arena = g->arena.as<uint32_t>();
+  a.arena = g->ws->arena.as<uint32_t>();
   if ((st = lb_prepare(g, a.L.lb, warps, (uint32_t)(kMotifHdr + kMaxK), &a.L, s))) return st;
   a.idle_min = (int)((1.0 - cfg->lb_threshold) * warps);
   if (a.idle_min < 1) a.idle_min = 1;
@@ -484,46 +484,42 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
     return fail(WM_EINVAL, "motif kernel packs vertex ids in %d bits; n=%lld too large for k=%d",
                 vbits, (long long)n, k);
   int st;
-  if ((st = g->outdeg.ensure(sizeof(int32_t) * (n + 1)))) return st;
-  if ((st = g->keys_in.ensure(sizeof(uint32_t) * n))) return st;
-  if ((st = g->keys_out.ensure(sizeof(uint32_t) * n))) return st;
-  if ((st = g->vals_in.ensure(sizeof(int32_t) * n))) return st;
-  if ((st = g->vals_out.ensure(sizeof(int32_t) * n))) return st;
-  if ((st = g->counters.ensure(sizeof(unsigned long long) * 64))) return st;
-  if ((st = g->lb.ensure(sizeof(LbState) * 8))) return st;
-  if ((st = g->table.ensure(sizeof(uint32_t) * app->dict_len))) return st;
-  if ((st = g->hist.ensure(sizeof(unsigned long long) * app->pattern_count))) return st;
+  if ((st = g->ws->outdeg.ensure(sizeof(int32_t) * (n + 1)))) return st;
+  if ((st = g->ws->keys_in.ensure(sizeof(uint32_t) * n))) return st;
+  if ((st = g->ws->keys_out.ensure(sizeof(uint32_t) * n))) return st;
+  if ((st = g->ws->vals_in.ensure(sizeof(int32_t) * n))) return st;
+  if ((st = g->ws->vals_out.ensure(sizeof(int32_t) * n))) return st;
+  if ((st = g->ws->counters.ensure(sizeof(unsigned long long) * 64))) return st;
+  if ((st = g->ws->lb.ensure(sizeof(LbState) * 8))) return st;
+  if ((st = g->ws->table.ensure(sizeof(uint32_t) * app->dict_len))) return st;
+  if ((st = g->ws->hist.ensure(sizeof(unsigned long long) * app->pattern_count))) return st;
   size_t tmp_sort = 0;
   WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
-      nullptr, tmp_sort, g->keys_in.as<uint32_t>(), g->keys_out.as<uint32_t>(),
-      g->vals_in.as<int32_t>(), g->vals_out.as<int32_t>(), (int)n, 0, 32, s));
-  if ((st = g->cub_tmp.ensure(tmp_sort))) return st;
+      nullptr, tmp_sort, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
+      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0, 32, s));
+  if ((st = g->ws->cub_tmp.ensure(tmp_sort))) return st;
 
-  cudaEvent_t e0, e1, k0, k1;
-  WM_CUDA(cudaEventCreate(&e0));
-  WM_CUDA(cudaEventCreate(&e1));
-  WM_CUDA(cudaEventCreate(&k0));
-  WM_CUDA(cudaEventCreate(&k1));
+  cudaEvent_t e0 = g->ws->ev[0], e1 = g->ws->ev[1], k0 = g->ws->ev[2], k1 = g->ws->ev[3];
   WM_CUDA(cudaEventRecord(e0, s));
-  unsigned long long *ctr = g->counters.as<unsigned long long>();
+  unsigned long long *ctr = g->ws->counters.as<unsigned long long>();
   WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
-  WM_CUDA(cudaMemsetAsync(g->hist.ptr, 0, sizeof(unsigned long long) * app->pattern_count, s));
-  WM_CUDA(cudaMemcpyAsync(g->table.ptr, app->dict_table, sizeof(uint32_t) * app->dict_len,
+  WM_CUDA(cudaMemsetAsync(g->ws->hist.ptr, 0, sizeof(unsigned long long) * app->pattern_count, s));
+  WM_CUDA(cudaMemcpyAsync(g->ws->table.ptr, app->dict_table, sizeof(uint32_t) * app->dict_len,
                           cudaMemcpyHostToDevice, s));
   const int tpb = 256;
   const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
                                 ? (n + tpb - 1) / tpb
                                 : (int64_t)g->num_sms * 16);
-  degree_kernel<<<eblocks, tpb, 0, s>>>(n, g->offsets, g->outdeg.as<int32_t>());
+  degree_kernel<<<eblocks, tpb, 0, s>>>(n, g->offsets, g->ws->outdeg.as<int32_t>());
   const int64_t rb = cfg->root_begin < 0 ? 0 : cfg->root_begin;
   const int64_t re = (cfg->root_end < 0 || cfg->root_end > n) ? n : cfg->root_end;
-  motif_task_keys_kernel<<<eblocks, tpb, 0, s>>>(n, g->outdeg.as<int32_t>(), rb, re,
-                                                 g->keys_in.as<uint32_t>(),
-                                                 g->vals_in.as<int32_t>(), ctr + 8);
-  size_t tb = g->cub_tmp.bytes;
+  motif_task_keys_kernel<<<eblocks, tpb, 0, s>>>(n, g->ws->outdeg.as<int32_t>(), rb, re,
+                                                 g->ws->keys_in.as<uint32_t>(),
+                                                 g->ws->vals_in.as<int32_t>(), ctr + 8);
+  size_t tb = g->ws->cub_tmp.bytes;
   WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
-      g->cub_tmp.ptr, tb, g->keys_in.as<uint32_t>(), g->keys_out.as<uint32_t>(),
-      g->vals_in.as<int32_t>(), g->vals_out.as<int32_t>(), (int)n, 0, 32, s));
+      g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
+      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0, 32, s));
   unsigned long long ntask = 0;
   WM_CUDA(cudaMemcpyAsync(&ntask, ctr + 8, sizeof ntask, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
@@ -531,24 +527,24 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   MotifArgs a;
   a.off = g->offsets;
   a.nbr = g->neighbors;
-  a.tasks = g->vals_out.as<int32_t>();
+  a.tasks = g->ws->vals_out.as<int32_t>();
   a.task_offset = (unsigned long long)cfg->shard_rank;
   a.task_stride = (unsigned long long)cfg->shard_count;
   a.ntasks = ntask > a.task_offset ? (ntask - a.task_offset + a.task_stride - 1) / a.task_stride : 0;
   a.k = k;
   a.vbits = vbits;
   a.vmask = (1u << vbits) - 1u;
-  a.table = g->table.as<uint32_t>();
+  a.table = g->ws->table.as<uint32_t>();
   a.pattern_count = app->pattern_count;
   a.maxdeg = g->max_degree > 0 ? g->max_degree : 1;
   a.warp_stride = (unsigned long long)a.maxdeg * (unsigned long long)((k - 2) * (k - 1) / 2);
-  a.hist = g->hist.as<unsigned long long>();
+  a.hist = g->ws->hist.as<unsigned long long>();
   a.counters = ctr;
   a.lb_on = lb_on;
   a.lb_poll = cfg->lb_poll > 0 ? cfg->lb_poll : 1;
   a.idle_min = 1;
   a.smem_hist = app->pattern_count <= 2048;
-  a.L.lb = g->lb.as<LbState>();
+  a.L.lb = g->ws->lb.as<LbState>();
   int warps = 0;
   if (a.ntasks) {
     st = bytes ? launch_motif<true>(g, cfg, a, s, &warps, false)
@@ -565,7 +561,7 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   WM_CUDA(cudaEventRecord(k1, s));
   unsigned long long hc[8];
   WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
-  WM_CUDA(cudaMemcpyAsync(res->pattern_counts, g->hist.ptr,
+  WM_CUDA(cudaMemcpyAsync(res->pattern_counts, g->ws->hist.ptr,
                           sizeof(unsigned long long) * app->pattern_count,
                           cudaMemcpyDeviceToHost, s));
   LbState hl;
@@ -575,10 +571,6 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   float kms = 0, dms = 0;
   WM_CUDA(cudaEventElapsedTime(&kms, k0, k1));
   WM_CUDA(cudaEventElapsedTime(&dms, e0, e1));
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaEventDestroy(k0);
-  cudaEventDestroy(k1);
   res->h2d_bytes = sizeof(uint32_t) * app->dict_len;
   res->d2h_bytes = sizeof ntask + sizeof hc + sizeof(unsigned long long) * app->pattern_count +
                    sizeof hl;
