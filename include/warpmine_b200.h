@@ -17,6 +17,8 @@
  *   WM_ECAPACITY   -> CapacityError           (engine.py:319-323)
  *   WM_EINVARIANT  -> InternalInvariantError  (engine.py:258-261, :472-473;
  *                                              aggregate.py:190-193)
+ *   WM_ESHUTDOWN   -> StoreShutdownError      (aggregate.py:88-99: the store
+ *                                              consumer is gone)
  *   WM_ECUDA       -> DeviceError (RuntimeError); no reference counterpart.
  */
 #ifndef WARPMINE_B200_H
@@ -35,6 +37,7 @@ extern "C" {
 #define WM_ECAPACITY (-2)
 #define WM_EINVARIANT (-3)
 #define WM_ECUDA (-4)
+#define WM_ESHUTDOWN (-5)
 
 /* Pipeline filter tags (engine.py:227-237); order-insensitive bit set. */
 #define WM_F_LOWER 1u
@@ -44,6 +47,7 @@ extern "C" {
 
 #define WM_AGG_COUNTER 0 /* aggregate_counter, aggregate.py:169-171 */
 #define WM_AGG_PATTERN 1 /* aggregate_pattern, aggregate.py:174-196 */
+#define WM_AGG_STORE 2   /* aggregate_store, aggregate.py:199-223 (wm_run_listing) */
 
 #define WM_MODE_WC 1  /* warp-centric, load balancing off  (engine.py:18-19) */
 #define WM_MODE_OPT 2 /* warp-centric + on-device balancer (engine.py:20-21) */
@@ -114,6 +118,52 @@ typedef struct {
   int warps;                    /* resident warps of the enumeration kernel */
   int bucket_words;             /* clique bitmap words per row (max bucket) */
 } wm_result;
+
+/* ---- subgraph listing (listing_app / subgraph_listing, apps.py:61-67,
+ * :94-118; aggregate_store, aggregate.py:199-223) ------------------------
+ *
+ * Every completed k-subgraph is streamed to the host as one record through a
+ * bounded ring in mapped pinned memory: producers (device warps) block while
+ * the ring is full, exactly the StoreBuffer back-pressure of
+ * aggregate.py:69-147.  The calling thread drains the ring and hands batches
+ * of records to `sink`; a non-zero return from `sink` is the dead consumer of
+ * aggregate.py:88-99: producers stop and wm_run_listing returns WM_ESHUTDOWN.
+ *
+ * Record layout (u32 words, `stride` words per record):
+ *   [0] sequence (internal)      [1] e, the k-th vertex
+ *   [2] mask: bit j set iff tr[j] is adjacent to e (adjacency_mask, :160-166)
+ *   [3] prefix bitmap low word   [4] prefix bitmap high word  (bitmap of tr[0..k-1))
+ *   [5 .. 5+k-1) tr[0..k-1)      (traversal order)
+ * The reference record is (tr[0..k-1) + (e,), bits) with
+ *   bits = prefix | mask << ((k-1)(k-2)/2 - 1)          (extend_bits, canon.py:76-90)
+ * which needs up to 65 bits at k = 12, so it is left to the consumer.
+ *
+ * Record checksum (order-independent, for parity at scale): with
+ *   smix(x) = splitmix64 finaliser of x + 0x9E3779B97F4A7C15,
+ *   h = 0; for v in vertices: h = smix(h ^ v);
+ *   h = smix(h ^ (bits mod 2^64)); h = smix(h ^ (bits >> 64)),
+ * checksum = sum of h over all emitted records mod 2^64. */
+#define WM_LIST_ALL 0      /* emit every connected induced k-subgraph */
+#define WM_LIST_COMPLETE 1 /* device-side complete_subgraph predicate (apps.py:121-123) */
+
+typedef int (*wm_sink_fn)(void *user, const uint32_t *records, uint64_t count,
+                          uint32_t stride_words);
+
+typedef struct {
+  uint32_t capacity;        /* ring records (rounded up to a power of two) */
+  uint32_t filter;          /* WM_LIST_* */
+  wm_sink_fn sink;          /* NULL: records are only counted and checksummed */
+  void *user;
+  uint64_t emitted;         /* out: records handed to the consumer */
+  uint64_t checksum;        /* out: record checksum (above) */
+  uint32_t stride_words;    /* out: record stride */
+  uint32_t reserved;
+} wm_listing;
+
+/* engine.run with the store aggregator (listing_app pipeline: extend(0,len),
+ * canonical, store).  Blocks until every record has been consumed. */
+int wm_run_listing(void *graph, const wm_app *app, const wm_cfg *cfg, wm_listing *listing,
+                   wm_result *result);
 
 /* Upload a CSR graph to the current device (cudaSetDevice beforehand). */
 int wm_graph_create(const wm_csr *csr, void **graph);

@@ -46,6 +46,9 @@ def lib():
                                     _u64p, _u64p, _u64p, _i64p, _u64p]
         L.wmo_clique_fast.argtypes = [ctypes.c_int64, _i64p, _i32p, ctypes.c_int, ctypes.c_int,
                                       _u64p, _u64p]
+        L.wmo_list_run.argtypes = [ctypes.c_int64, _i64p, _i32p, ctypes.c_int, ctypes.c_int,
+                                   ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                                   _u64p, _u64p, _u64p]
         _LIB = L
     return _LIB
 
@@ -102,6 +105,41 @@ def motif_run(g, k, table, pattern_count, root_begin=-1, root_end=-1, roots=None
         raise _ERR.get(st, RuntimeError)("oracle status %d" % st)
     return {"hist": [int(x) for x in hist], "leaves": leaves.value, "alg_bytes": ab.value,
             "roots_done": done.value, "nodes": nodes.value}
+
+
+def list_run(g, k, complete_only=False, root_begin=-1, root_end=-1, threads=None):
+    """Reference listing_app pipeline; returns dict with leaves, emitted and
+    the order-independent record checksum (include/warpmine_b200.h)."""
+    off, nbr = _arrays(g)
+    lv, em, cs = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    st = lib().wmo_list_run(g.n, off.ctypes.data_as(_i64p), nbr.ctypes.data_as(_i32p), k,
+                            int(complete_only), root_begin, root_end, threads or os.cpu_count(),
+                            ctypes.byref(lv), ctypes.byref(em), ctypes.byref(cs))
+    if st:
+        raise _ERR.get(st, RuntimeError)("oracle status %d" % st)
+    return {"leaves": lv.value, "emitted": em.value, "checksum": cs.value}
+
+
+def record_checksum(records):
+    """The checksum of include/warpmine_b200.h over (vertices, bits) records
+    (pure Python; for golden fixtures and small cross-checks)."""
+    M = (1 << 64) - 1
+
+    def smix(x):
+        x = (x + 0x9E3779B97F4A7C15) & M
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & M
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & M
+        return x ^ (x >> 31)
+
+    total = 0
+    for vertices, bits in records:
+        h = 0
+        for v in vertices:
+            h = smix(h ^ int(v))
+        h = smix(h ^ (bits & M))
+        h = smix(h ^ (bits >> 64))
+        total = (total + h) & M
+    return total
 
 
 def clique_fast(g, k, threads=None, with_bytes=False):

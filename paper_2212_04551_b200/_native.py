@@ -11,19 +11,20 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import CapacityError, DeviceError, InternalInvariantError
+from .errors import CapacityError, DeviceError, InternalInvariantError, StoreShutdownError
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libwm_b200.so")
 
-WM_OK, WM_EINVAL, WM_ECAPACITY, WM_EINVARIANT, WM_ECUDA = 0, -1, -2, -3, -4
+WM_OK, WM_EINVAL, WM_ECAPACITY, WM_EINVARIANT, WM_ECUDA, WM_ESHUTDOWN = 0, -1, -2, -3, -4, -5
 WM_F_LOWER, WM_F_COMPACT, WM_F_CLIQUE, WM_F_CANONICAL = 1, 2, 4, 8
-WM_AGG_COUNTER, WM_AGG_PATTERN = 0, 1
+WM_AGG_COUNTER, WM_AGG_PATTERN, WM_AGG_STORE = 0, 1, 2
+WM_LIST_ALL, WM_LIST_COMPLETE = 0, 1
 WM_MODE_WC, WM_MODE_OPT = 1, 2
 WM_ORDER_ID, WM_ORDER_DEGREE = 0, 1
 
-EXPORTED = ("wm_graph_create", "wm_graph_create_device", "wm_run", "wm_graph_destroy",
-            "wm_last_error", "wm_abi_version")
+EXPORTED = ("wm_graph_create", "wm_graph_create_device", "wm_run", "wm_run_listing",
+            "wm_graph_destroy", "wm_last_error", "wm_abi_version")
 
 
 class WmCsr(ctypes.Structure):
@@ -63,6 +64,18 @@ class WmResult(ctypes.Structure):
                 ("warps", ctypes.c_int), ("bucket_words", ctypes.c_int)]
 
 
+# int (*wm_sink_fn)(void *user, const uint32_t *records, uint64_t count, uint32_t stride)
+SINK_FN = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_void_p, ctypes.POINTER(ctypes.c_uint32),
+                           ctypes.c_uint64, ctypes.c_uint32)
+
+
+class WmListing(ctypes.Structure):
+    _fields_ = [("capacity", ctypes.c_uint32), ("filter", ctypes.c_uint32),
+                ("sink", SINK_FN), ("user", ctypes.c_void_p),
+                ("emitted", ctypes.c_uint64), ("checksum", ctypes.c_uint64),
+                ("stride_words", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
+
+
 _LIB = None
 
 
@@ -83,6 +96,9 @@ def load():
     L.wm_run.argtypes = [ctypes.c_void_p, ctypes.POINTER(WmApp), ctypes.POINTER(WmCfg),
                          ctypes.POINTER(WmResult)]
     L.wm_run.restype = ctypes.c_int
+    L.wm_run_listing.argtypes = [ctypes.c_void_p, ctypes.POINTER(WmApp), ctypes.POINTER(WmCfg),
+                                 ctypes.POINTER(WmListing), ctypes.POINTER(WmResult)]
+    L.wm_run_listing.restype = ctypes.c_int
     L.wm_graph_destroy.argtypes = [ctypes.c_void_p]
     L.wm_graph_destroy.restype = None
     L.wm_last_error.argtypes = []
@@ -103,4 +119,6 @@ def check(status: int) -> None:
         raise CapacityError(msg)
     if status == WM_EINVARIANT:
         raise InternalInvariantError(msg)
+    if status == WM_ESHUTDOWN:
+        raise StoreShutdownError(msg)
     raise DeviceError(msg or "libwm_b200 status %d" % status)

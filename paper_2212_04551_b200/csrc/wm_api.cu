@@ -272,11 +272,9 @@ void wm_graph_destroy(void *gp) {
   delete g;
 }
 
-int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
-  g_last_error.clear();
-  Graph *g = static_cast<Graph *>(gp);
+// engine.py:791-798 / balance.py:48-52, shared by wm_run and wm_run_listing
+static int check_run_args(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
   if (!g || !app || !cfg || !res) return fail(WM_EINVAL, "null argument");
-  // engine.py:791-798 / balance.py:48-52
   if (cfg->mode != WM_MODE_WC && cfg->mode != WM_MODE_OPT)
     return fail(WM_EINVAL, "mode must be wc or opt (dfs has no device path)");
   if (cfg->mode == WM_MODE_OPT && !(cfg->lb_threshold > 0.0 && cfg->lb_threshold <= 1.0))
@@ -287,6 +285,18 @@ int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
     return fail(WM_EINVAL, "bad shard %d/%d", cfg->shard_rank, cfg->shard_count);
   // engine.py:72-80, apps.py:38-58
   if (app->k < 3) return fail(WM_EINVAL, "need k >= 3");
+  int dev = 0;
+  WM_CUDA(cudaGetDevice(&dev));
+  if (dev != g->device)
+    return fail(WM_EINVAL, "graph lives on device %d, current device is %d", g->device, dev);
+  return WM_OK;
+}
+
+int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
+  g_last_error.clear();
+  Graph *g = static_cast<Graph *>(gp);
+  int st = check_run_args(g, app, cfg, res);
+  if (st) return st;
   const bool clique = app->aggregator == WM_AGG_COUNTER && !app->extend_all &&
                       (app->filters & WM_F_CLIQUE) && (app->filters & WM_F_LOWER) &&
                       !(app->filters & WM_F_CANONICAL);
@@ -296,10 +306,6 @@ int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
   memset(res, 0, sizeof *res);
   res->pattern_counts = user_hist;
   cudaStream_t s = cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : g->ws->own_stream;
-  int dev = 0;
-  WM_CUDA(cudaGetDevice(&dev));
-  if (dev != g->device)
-    return fail(WM_EINVAL, "graph lives on device %d, current device is %d", g->device, dev);
   if (clique) {
     if (app->k > 12) return fail(WM_EINVAL, "k must be in [3, 12], got %d", app->k);
     return run_clique(g, app, cfg, res, s);
@@ -312,9 +318,34 @@ int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
     if (!user_hist) return fail(WM_EINVAL, "pattern_counts buffer required");
     return run_motif(g, app, cfg, res, s);
   }
+  if (app->aggregator == WM_AGG_STORE)
+    return fail(WM_EINVAL, "store aggregation runs through wm_run_listing");
   return fail(WM_EINVAL,
               "pipeline not supported on the device: only the built-in clique_app and "
               "motif_app pipelines run (no CPU fallback)");
+}
+
+int wm_run_listing(void *gp, const wm_app *app, const wm_cfg *cfg, wm_listing *lst,
+                   wm_result *res) {
+  g_last_error.clear();
+  Graph *g = static_cast<Graph *>(gp);
+  int st = check_run_args(g, app, cfg, res);
+  if (st) return st;
+  if (!lst) return fail(WM_EINVAL, "null listing");
+  // listing_app (apps.py:61-67): extend(0,len), canonical, store
+  if (!(app->aggregator == WM_AGG_STORE && app->extend_all && app->genedges &&
+        app->filters == WM_F_CANONICAL))
+    return fail(WM_EINVAL, "wm_run_listing needs the listing_app pipeline");
+  if (app->k > 12) return fail(WM_EINVAL, "k must be in [3, 12], got %d", app->k);
+  if (lst->capacity < 1) return fail(WM_EINVAL, "capacity must be positive");
+  if (lst->filter != WM_LIST_ALL && lst->filter != WM_LIST_COMPLETE)
+    return fail(WM_EINVAL, "unknown listing filter %u", lst->filter);
+  if (cfg->count_bytes) return fail(WM_EINVAL, "count_bytes is not available for listing");
+  memset(res, 0, sizeof *res);
+  lst->emitted = 0;
+  lst->checksum = 0;
+  cudaStream_t s = cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : g->ws->own_stream;
+  return run_motif(g, app, cfg, res, s, lst);
 }
 
 }  // extern "C"

@@ -321,7 +321,8 @@ struct Graph {
 int lb_prepare(Graph *g, LbState *lb, int warps, uint32_t words, LbShared *out, cudaStream_t s);
 
 int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s);
-int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s);
+int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s,
+              wm_listing *lst = nullptr);
 
 // fills the idle fractions and LB stats of `res` from a device LbState copy
 void finish_lb_stats(const LbState &h, wm_result *res);

@@ -59,6 +59,22 @@ __global__ void motif_task_keys_kernel(int64_t n, const int32_t *__restrict__ de
   }
 }
 
+// Listing ring (aggregate_store, aggregate.py:199-223): records go to mapped
+// pinned host memory; `head` (device) hands out record tickets, ctl[0] (host)
+// is the consumer's tail, ctl[1] its failure flag.  A producer blocks while
+// its ticket is more than `cap` ahead of the tail (StoreBuffer back-pressure,
+// aggregate.py:69-99).
+struct ListRing {
+  uint32_t *slots;                 // host-mapped [cap * stride]
+  unsigned long long *ctl;         // host-mapped [0] tail [1] failed
+  unsigned long long *head;        // device ticket counter
+  unsigned long long cap_mask;
+  uint32_t stride;                 // words per record (k + 4)
+  uint32_t filter;                 // WM_LIST_*
+  unsigned long long full_prefix;  // bitmap of a complete (k-1)-prefix
+  uint32_t full_mask;              // mask of e adjacent to all of tr[0..k-1)
+};
+
 struct MotifArgs {
   const int64_t *off;
   const int32_t *nbr;
@@ -77,12 +93,16 @@ struct MotifArgs {
   int lb_on, lb_poll, idle_min;
   int smem_hist;
   LbShared L;
+  ListRing ring;
 };
 
 struct MotifWarp {
   int32_t tr[kMaxK];
   long long tb[kMaxK], te[kMaxK];   // CSR row bounds of tr[j]
-  uint32_t bm[kMaxK];               // bm[L-1] = bitmap of tr[0..L)
+  unsigned long long bm[kMaxK];     // bm[L-1] = bitmap of tr[0..L) (<= 54 bits, k <= 12)
+  unsigned long long tail_cache;    // listing: last consumer tail seen (lane 0)
+  int32_t le[32];                   // listing: leaf vertex of record rank r
+  uint32_t lm[32];                  //          and its adjacency mask
   uint32_t size[kMaxK], cur[kMaxK], lo[kMaxK];
   unsigned long long below[kMaxK];  // leaves under the node of length L
 };
@@ -198,7 +218,7 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
   const int32_t x = w.tr[L];
   const long long xb = w.tb[L], xe = w.te[L];
   const int32_t t0 = w.tr[0];
-  const uint32_t bits = w.bm[L];  // bitmap of tr[0..k-1)
+  const uint32_t bits = (uint32_t)w.bm[L];  // bitmap of tr[0..k-1) (k <= 8 here)
   const int off = group_off(a.k - 1);
   const uint32_t n_src = w.size[L];
   unsigned long long total = 0;
@@ -249,6 +269,138 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
   return total + nb;
 }
 
+
+using aref_sys_u64 = cuda::atomic_ref<unsigned long long, cuda::thread_scope_system>;
+using aref_sys_u32 = cuda::atomic_ref<uint32_t, cuda::thread_scope_system>;
+
+// Warp-collective: stream one record per lane with `keep` (leaf e with
+// adjacency mask) to the host ring, in rank order.  Returns false once the
+// consumer has failed (aggregate.py:88-99); the warp then stops producing.
+__device__ __forceinline__ bool emit_records(const MotifArgs &a, MotifWarp &w, bool keep,
+                                             int32_t e, uint32_t mask) {
+  const ListRing &R = a.ring;
+  const int lane = lane_id();
+  const unsigned bal = __ballot_sync(0xffffffffu, keep);
+  if (!bal) return true;
+  const int n = __popc(bal);
+  const int rank = __popc(bal & ((1u << lane) - 1u));
+  if (keep) {
+    w.le[rank] = e;
+    w.lm[rank] = mask;
+  }
+  unsigned long long base = 0;
+  int ok = 1;
+  if (lane == 0) {
+    base = atomicAdd(R.head, (unsigned long long)n);
+    // back-pressure: tickets [base, base+n) need free slots.  The consumer's
+    // tail lives in host memory; it is read only when the cached copy says
+    // the ring may be full.
+    const unsigned long long need = base + (unsigned long long)n;
+    unsigned sl = 128;
+    while (need > w.tail_cache + R.cap_mask + 1ull) {
+      w.tail_cache = aref_sys_u64(R.ctl[0]).load(cuda::std::memory_order_relaxed);
+      if (need <= w.tail_cache + R.cap_mask + 1ull) break;
+      if (aref_sys_u64(R.ctl[1]).load(cuda::std::memory_order_relaxed) ||
+          ld_relaxed(&a.L.lb->error)) {
+        ok = 0;
+        break;
+      }
+      __nanosleep(sl);
+      if (sl < 8192) sl <<= 1;
+    }
+  }
+  ok = __shfl_sync(0xffffffffu, ok, 0);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (!ok) {
+    if (lane == 0) raise_error(a.L.lb, WM_ESHUTDOWN);
+    return false;
+  }
+  __syncwarp();
+  // record payload, coalesced over the warp (word 0, the sequence, last)
+  const uint32_t st = R.stride;
+  const int nw = n * (int)st;
+  const unsigned long long bm = w.bm[a.k - 2];
+  for (int i = lane; i < nw; i += 32) {
+    const int r = i / (int)st, j = i - r * (int)st;
+    if (j == 0) continue;
+    uint32_t v;
+    if (j == 1) v = (uint32_t)w.le[r];
+    else if (j == 2) v = w.lm[r];
+    else if (j == 3) v = (uint32_t)bm;
+    else if (j == 4) v = (uint32_t)(bm >> 32);
+    else v = (uint32_t)w.tr[j - 5];
+    R.slots[((base + (unsigned long long)r) & R.cap_mask) * st + j] = v;
+  }
+  __threadfence_system();
+  __syncwarp();
+  if (keep) {
+    const unsigned long long idx = base + (unsigned long long)rank;
+    aref_sys_u32(R.slots[(idx & R.cap_mask) * st])
+        .store((uint32_t)(idx + 1ull), cuda::std::memory_order_relaxed);
+  }
+  __syncwarp();
+  return true;
+}
+
+// listing leaves of tr[0..k-1): same candidates as aggregate_leaves, every
+// one streamed as a record (aggregate_store, aggregate.py:199-223).  Returns
+// the leaves found (aggregated_total); *emitted counts records that passed
+// the device filter; *ok turns false when the consumer failed.
+__device__ __forceinline__ unsigned long long list_leaves(const MotifArgs &a, MotifWarp &w,
+                                                          uint32_t *base,
+                                                          unsigned long long &emitted,
+                                                          bool &ok) {
+  const int lane = lane_id();
+  const int L = a.k - 2;
+  const uint32_t *src = level_ptr(a, base, L);
+  const int32_t x = w.tr[L];
+  const long long xb = w.tb[L], xe = w.te[L];
+  const int32_t t0 = w.tr[0];
+  const uint32_t n_src = w.size[L];
+  const bool complete_only = a.ring.filter == WM_LIST_COMPLETE;
+  const bool prefix_full = w.bm[L] == a.ring.full_prefix;
+  unsigned long long total = 0;
+  for (uint32_t i0 = 0; i0 < n_src && ok; i0 += 32) {
+    const uint32_t i = i0 + lane;
+    bool valid = false;
+    int32_t e = 0;
+    uint32_t mask = 0;
+    if (i < n_src) {
+      const uint32_t ent = __ldcg(src + i);
+      e = (int32_t)(ent & a.vmask);
+      if (e > x) {
+        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
+        mask = (ent >> a.vbits) | ((uint32_t)adj_probe(a.nbr, e, eb, ee, x, xb, xe) << L);
+        valid = true;
+      }
+    }
+    total += __popc(__ballot_sync(0xffffffffu, valid));
+    const bool keep = valid && (!complete_only || (prefix_full && mask == a.ring.full_mask));
+    emitted += __popc(__ballot_sync(0xffffffffu, keep));
+    ok = emit_records(a, w, keep, e, mask);
+  }
+  // B part (mask = 1 << L: e sees only tr[L], never complete for k >= 3)
+  for (long long p0 = xb; p0 < xe && ok; p0 += 32) {
+    const long long p = p0 + lane;
+    bool keep = false;
+    int32_t e = 0;
+    if (p < xe) {
+      e = __ldg(a.nbr + p);
+      if (e > t0) {
+        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
+        keep = true;
+        for (int j = 0; j < L && keep; ++j)
+          keep = !adj_probe(a.nbr, e, eb, ee, w.tr[j], w.tb[j], w.te[j]);
+      }
+    }
+    total += __popc(__ballot_sync(0xffffffffu, keep));
+    const bool out = keep && (!complete_only || (prefix_full && (1u << L) == a.ring.full_mask));
+    emitted += __popc(__ballot_sync(0xffffffffu, out));
+    ok = emit_records(a, w, out, e, 1u << L);
+  }
+  return total;
+}
+
 __device__ __forceinline__ void set_tr(const MotifArgs &a, MotifWarp &w, int j, int32_t v) {
   if (lane_id() == 0) {
     w.tr[j] = v;
@@ -258,9 +410,9 @@ __device__ __forceinline__ void set_tr(const MotifArgs &a, MotifWarp &w, int j, 
   __syncwarp();
 }
 
-constexpr int kMotifHdr = 5;  // [root, level, lo, hi, bitmap] then tr[1..level)
+constexpr int kMotifHdr = 6;  // [root, level, lo, hi, bitmap lo, bitmap hi] then tr[1..level)
 
-template <bool BYTES>
+template <bool BYTES, bool LIST>
 __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned long long *sh = reinterpret_cast<unsigned long long *>(smraw);
@@ -279,8 +431,11 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
   warp_clock_begin(clk, a.L.lb);
   bool roots_left = true;
   unsigned long long leaves = 0, bytes = 0, tasks_done = 0, nodes = 0, polls = 0, peak = 0;
+  unsigned long long emitted = 0;
+  bool ok = true;
+  if (LIST && lane == 0) w.tail_cache = 0;
   int poll = 0;
-  for (;;) {
+  while (ok) {
     unsigned long long ti = 0;
     Rec3 rec = {{0u, 0u, 0u}};
     const int kind = acquire_work(a.L, a.lb_on, a.ntasks, roots_left, ti, rec, clk);
@@ -304,7 +459,9 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
     } else {
       // donated prefix: rebuild E_1..E_s0 deterministically, then own [lo, hi)
       s0 = (int)rec_word(rec, 1);
-      const uint32_t lo = rec_word(rec, 2), hi = rec_word(rec, 3), bm = rec_word(rec, 4);
+      const uint32_t lo = rec_word(rec, 2), hi = rec_word(rec, 3);
+      const unsigned long long bm =
+          (unsigned long long)rec_word(rec, 4) | ((unsigned long long)rec_word(rec, 5) << 32);
       set_tr(a, w, 0, (int32_t)rec_word(rec, 0));
       for (int j = 1; j < s0; ++j) set_tr(a, w, j, (int32_t)rec_word(rec, kMotifHdr + j - 1));
       uint32_t n = build_first(a, w, base);
@@ -348,12 +505,19 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
       if (lane == 0) {
         w.cur[s] = cur - 1;
         // induce (engine.py:678-705): bitmap of tr[0..s] (s+1 vertices)
-        w.bm[s] = (s == 1) ? 0u : (w.bm[s - 1] | (m << group_off(s)));
+        w.bm[s] = (s == 1) ? 0ull
+                           : (w.bm[s - 1] | ((unsigned long long)m << group_off(s)));
       }
       __syncwarp();
       ++nodes;
       if (s + 1 == k - 1) {
-        const unsigned long long got = aggregate_leaves(a, w, base, sh);
+        unsigned long long got;
+        if (LIST) {
+          got = list_leaves(a, w, base, emitted, ok);
+          if (!ok) break;
+        } else {
+          got = aggregate_leaves(a, w, base, sh);
+        }
         leaves += got;
         if (BYTES && lane == 0 && got) {
           bytes += 4ull * (unsigned long long)(w.te[s] - w.tb[s]);
@@ -399,7 +563,8 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
                 else if (idx == 1) val = (uint32_t)sd;
                 else if (idx == 2) val = lo;
                 else if (idx == 3) val = lo + half;
-                else if (idx == 4) val = w.bm[sd - 1];
+                else if (idx == 4) val = (uint32_t)w.bm[sd - 1];
+                else if (idx == 5) val = (uint32_t)(w.bm[sd - 1] >> 32);
                 else if (idx >= kMotifHdr && idx < kMotifHdr + sd - 1) val = (uint32_t)w.tr[idx - kMotifHdr + 1];
                 r.w[q] = val;
               }
@@ -424,6 +589,7 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
     atomicAdd(&a.counters[3], nodes);
     atomicAdd(&a.counters[4], polls);
     atomicMax(&a.counters[5], peak);
+    if (LIST) atomicAdd(&a.counters[6], emitted);
   }
   warp_clock_end(a.L.lb, clk);
   if (a.smem_hist) {
@@ -433,13 +599,13 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
   }
 }
 
-template <bool BYTES>
+template <bool BYTES, bool LIST>
 static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s, int *warps_out,
                         bool launch) {
   int wpb = cfg->warps_per_block > 0 ? cfg->warps_per_block : 8;
   const size_t hist_bytes = a.smem_hist ? ((size_t)a.pattern_count * 8 + 15) / 16 * 16 : 0;
   const size_t smem = hist_bytes + sizeof(MotifWarp) * wpb;
-  auto kern = motif_enum_kernel<BYTES>;
+  auto kern = motif_enum_kernel<BYTES, LIST>;
   WM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int bps = 0;
   WM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
@@ -474,7 +640,117 @@ static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s
   return WM_OK;
 }
 
-int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s) {
+// Host side of the listing ring: mapped pinned memory cached in the
+// workspace, drained on the calling thread while the kernel runs.
+struct HostRing {
+  uint32_t *slots = nullptr;
+  unsigned long long *ctl = nullptr;
+  size_t bytes = 0;
+};
+static HostRing g_hring[64];
+
+static int host_ring_get(Graph *g, unsigned long long cap, uint32_t stride, HostRing **out) {
+  HostRing &h = g_hring[g->device];
+  const size_t want = 256 + sizeof(uint32_t) * (size_t)cap * stride;
+  if (h.bytes < want) {
+    if (h.ctl) cudaFreeHost(h.ctl);
+    h = HostRing();
+    void *p = nullptr;
+    WM_CUDA(cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable));
+    h.ctl = static_cast<unsigned long long *>(p);
+    h.slots = reinterpret_cast<uint32_t *>(static_cast<char *>(p) + 256);
+    h.bytes = want;
+  }
+  *out = &h;
+  return WM_OK;
+}
+
+// splitmix64 finaliser and the record checksum of include/warpmine_b200.h
+static inline uint64_t smix(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+static uint64_t record_hash(const uint32_t *r, int k) {
+  uint64_t h = 0;
+  for (int j = 0; j < k - 1; ++j) h = smix(h ^ (uint64_t)r[5 + j]);
+  h = smix(h ^ (uint64_t)r[1]);
+  const int off = (k - 1) * (k - 2) / 2 - 1;
+  const unsigned __int128 bits = ((unsigned __int128)r[3] | ((unsigned __int128)r[4] << 32)) |
+                                 ((unsigned __int128)r[2] << off);
+  h = smix(h ^ (uint64_t)bits);
+  h = smix(h ^ (uint64_t)(bits >> 64));
+  return h;
+}
+
+// Drain records until the kernel (event `done`) has finished and every
+// ticket it handed out is consumed.
+static int drain_listing(HostRing *h, unsigned long long cap, uint32_t stride, int k,
+                         wm_listing *lst, cudaEvent_t done) {
+  unsigned long long tail = 0;
+  const unsigned long long mask = cap - 1;
+  bool failed = false;
+  uint64_t sum = 0, emitted = 0;
+  int idle = 0;
+  const unsigned long long batch_max = cap / 4 > 0 ? cap / 4 : 1;
+  for (;;) {
+    unsigned long long avail = 0;
+    // after a sink failure the tail stops: producers block, see ctl[1], stop
+    while (!failed && avail < batch_max) {
+      const unsigned long long idx = tail + avail;
+      const uint32_t seq = __atomic_load_n(&h->slots[(idx & mask) * stride], __ATOMIC_ACQUIRE);
+      if (seq != (uint32_t)(idx + 1)) break;
+      ++avail;
+    }
+    if (avail) {
+      idle = 0;
+      // contiguous runs (the ring may wrap once inside the batch)
+      unsigned long long done_n = 0;
+      while (done_n < avail) {
+        const unsigned long long first = (tail + done_n) & mask;
+        unsigned long long run = avail - done_n;
+        if (first + run > cap) run = cap - first;
+        const uint32_t *recs = h->slots + first * stride;
+        if (!failed) {
+          for (unsigned long long r = 0; r < run; ++r) sum += record_hash(recs + r * stride, k);
+          emitted += run;
+          if (lst->sink && lst->sink(lst->user, recs, run, stride) != 0) {
+            failed = true;
+            __atomic_store_n(&h->ctl[1], 1ull, __ATOMIC_RELEASE);
+          }
+        }
+        done_n += run;
+      }
+      tail += avail;
+      __atomic_store_n(&h->ctl[0], tail, __ATOMIC_RELEASE);
+      continue;
+    }
+    const cudaError_t q = cudaEventQuery(done);
+    if (q == cudaSuccess) {
+      if (failed) break;  // records left in the ring are discarded
+      // the kernel is complete: everything it wrote is visible; one more pass
+      const unsigned long long idx = tail;
+      const uint32_t seq = __atomic_load_n(&h->slots[(idx & mask) * stride], __ATOMIC_ACQUIRE);
+      if (seq == (uint32_t)(idx + 1)) continue;
+      break;
+    }
+    if (q != cudaErrorNotReady) return fail(WM_ECUDA, "listing kernel failed: %s",
+                                           cudaGetErrorString(q));
+    if (++idle > 64) {
+      struct timespec ts = {0, 20000};
+      nanosleep(&ts, nullptr);
+    }
+  }
+  lst->emitted = emitted;
+  lst->checksum = sum;
+  lst->stride_words = stride;
+  return failed ? WM_ESHUTDOWN : WM_OK;
+}
+
+int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s,
+              wm_listing *lst) {
   const int64_t n = g->n;
   const int k = app->k;
   const bool bytes = cfg->count_bytes != 0;
@@ -503,9 +779,12 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   WM_CUDA(cudaEventRecord(e0, s));
   unsigned long long *ctr = g->ws->counters.as<unsigned long long>();
   WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
-  WM_CUDA(cudaMemsetAsync(g->ws->hist.ptr, 0, sizeof(unsigned long long) * app->pattern_count, s));
-  WM_CUDA(cudaMemcpyAsync(g->ws->table.ptr, app->dict_table, sizeof(uint32_t) * app->dict_len,
-                          cudaMemcpyHostToDevice, s));
+  if (!lst) {
+    WM_CUDA(cudaMemsetAsync(g->ws->hist.ptr, 0, sizeof(unsigned long long) * app->pattern_count,
+                            s));
+    WM_CUDA(cudaMemcpyAsync(g->ws->table.ptr, app->dict_table, sizeof(uint32_t) * app->dict_len,
+                            cudaMemcpyHostToDevice, s));
+  }
   const int tpb = 256;
   const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
                                 ? (n + tpb - 1) / tpb
@@ -545,25 +824,60 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   a.idle_min = 1;
   a.smem_hist = app->pattern_count <= 2048;
   a.L.lb = g->ws->lb.as<LbState>();
+  memset(&a.ring, 0, sizeof a.ring);
+  HostRing *hr = nullptr;
+  unsigned long long cap = 0;
+  if (lst) {
+    cap = 64;
+    while (cap < lst->capacity && cap < (1ull << 26)) cap <<= 1;
+    const uint32_t stride = (uint32_t)k + 4u;
+    if ((st = host_ring_get(g, cap, stride, &hr))) return st;
+    memset(hr->ctl, 0, 256);
+    for (unsigned long long i = 0; i < cap; ++i) hr->slots[i * stride] = 0u;
+    if ((st = g->ws->listing.ensure(sizeof(unsigned long long)))) return st;
+    WM_CUDA(cudaMemsetAsync(g->ws->listing.ptr, 0, sizeof(unsigned long long), s));
+    uint32_t *dslots = nullptr;
+    unsigned long long *dctl = nullptr;
+    WM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dslots), hr->slots, 0));
+    WM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dctl), hr->ctl, 0));
+    a.ring.slots = dslots;
+    a.ring.ctl = dctl;
+    a.ring.head = g->ws->listing.as<unsigned long long>();
+    a.ring.cap_mask = cap - 1;
+    a.ring.stride = stride;
+    a.ring.filter = lst->filter;
+    const int sp = (k - 1) * (k - 2) / 2 - 1;  // stored_bits(k-1), canon.py:42-48
+    a.ring.full_prefix = sp > 0 ? ((sp >= 64) ? ~0ull : ((1ull << sp) - 1ull)) : 0ull;
+    a.ring.full_mask = (1u << (k - 1)) - 1u;
+    a.smem_hist = 0;
+  }
   int warps = 0;
+#define WM_LAUNCH(GO)                                                            \
+  (bytes ? launch_motif<true, false>(g, cfg, a, s, &warps, GO)                   \
+         : (lst ? launch_motif<false, true>(g, cfg, a, s, &warps, GO)            \
+                : launch_motif<false, false>(g, cfg, a, s, &warps, GO)))
   if (a.ntasks) {
-    st = bytes ? launch_motif<true>(g, cfg, a, s, &warps, false)
-               : launch_motif<false>(g, cfg, a, s, &warps, false);
-    if (st) return st;
+    if ((st = WM_LAUNCH(false))) return st;
   }
   WM_CUDA(cudaEventRecord(k0, s));
   if (a.ntasks) {
-    st = bytes ? launch_motif<true>(g, cfg, a, s, &warps, true)
-               : launch_motif<false>(g, cfg, a, s, &warps, true);
-    if (st) return st;
+    if ((st = WM_LAUNCH(true))) return st;
     res->launches += 2;
   }
+#undef WM_LAUNCH
   WM_CUDA(cudaEventRecord(k1, s));
+  int drain_st = WM_OK;
+  if (lst) {
+    // consume while the kernel produces (the host copies below would block)
+    drain_st = drain_listing(hr, cap, a.ring.stride, k, lst, k1);
+    if (drain_st == WM_ECUDA) return drain_st;
+  }
   unsigned long long hc[8];
   WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
-  WM_CUDA(cudaMemcpyAsync(res->pattern_counts, g->ws->hist.ptr,
-                          sizeof(unsigned long long) * app->pattern_count,
-                          cudaMemcpyDeviceToHost, s));
+  if (!lst)
+    WM_CUDA(cudaMemcpyAsync(res->pattern_counts, g->ws->hist.ptr,
+                            sizeof(unsigned long long) * app->pattern_count,
+                            cudaMemcpyDeviceToHost, s));
   LbState hl;
   WM_CUDA(cudaMemcpyAsync(&hl, a.L.lb, sizeof hl, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaEventRecord(e1, s));
@@ -571,9 +885,10 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   float kms = 0, dms = 0;
   WM_CUDA(cudaEventElapsedTime(&kms, k0, k1));
   WM_CUDA(cudaEventElapsedTime(&dms, e0, e1));
-  res->h2d_bytes = sizeof(uint32_t) * app->dict_len;
-  res->d2h_bytes = sizeof ntask + sizeof hc + sizeof(unsigned long long) * app->pattern_count +
-                   sizeof hl;
+  res->h2d_bytes = lst ? 0 : sizeof(uint32_t) * app->dict_len;
+  res->d2h_bytes = sizeof ntask + sizeof hc + sizeof hl +
+                   (lst ? (uint64_t)lst->emitted * a.ring.stride * 4
+                        : sizeof(unsigned long long) * app->pattern_count);
   res->leaves = hc[0];
   res->alg_bytes = bytes ? hc[1] : 0;
   res->tasks = hc[2];
@@ -582,15 +897,19 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   res->kernel_ms = kms;
   res->device_ms = dms;
   res->warps = warps;
+  res->peak_ext = hc[5];
   if (a.ntasks) {
     finish_lb_stats(hl, res);
+    res->peak_ext = hc[5];
+    if (drain_st == WM_ESHUTDOWN || hl.error == WM_ESHUTDOWN)
+      return fail(WM_ESHUTDOWN, "store consumer terminated");
     if (hl.error) {
       return fail(hl.error, hl.error == WM_EINVARIANT
                                 ? "completed subgraph mapped to an unreachable bitmap"
                                 : "extension array exceeded its capacity");
     }
   }
-  res->peak_ext = hc[5];
+  if (drain_st) return fail(drain_st, "store consumer terminated");
   return WM_OK;
 }
 

@@ -37,6 +37,11 @@ from . import balance as bal
 from .graph import CsrGraph
 
 MODES = ("dfs", "wc", "opt")
+
+# Store target of ``apps.listing_checksum``: records are consumed inside the
+# native library (counted + checksummed) instead of a Python StoreBuffer.
+NATIVE_STORE = object()
+LISTING_RING = 1 << 16   # device->host ring records (the StoreBuffer keeps its own capacity)
 DEFAULT_WARPS = 4
 DEFAULT_LANE_WIDTH = 32
 _BUILTIN_TAGS = ("lower", "compact", "clique", "canonical")
@@ -185,13 +190,12 @@ def _app_struct(app: Application):
     for t in tags:
         flags |= {"lower": _native.WM_F_LOWER, "compact": _native.WM_F_COMPACT,
                   "clique": _native.WM_F_CLIQUE, "canonical": _native.WM_F_CANONICAL}[t]
-    if app.aggregator == "store":
-        raise ValueError("store aggregation (subgraph listing) has no device path yet")
     a = _native.WmApp()
     a.k = app.k
     a.extend_all = int(app.extend_all)
     a.genedges = int(app.genedges)
-    a.aggregator = _native.WM_AGG_COUNTER if app.aggregator == "counter" else _native.WM_AGG_PATTERN
+    a.aggregator = {"counter": _native.WM_AGG_COUNTER, "pattern": _native.WM_AGG_PATTERN,
+                    "store": _native.WM_AGG_STORE}[app.aggregator]
     a.filters = flags
     keep = None
     if app.aggregator == "pattern":
@@ -258,6 +262,8 @@ def run(g: CsrGraph, app: Application, *, mode: str = "wc", warps: int = None,
     cfg.blocks_per_sm = blocks_per_sm
     cfg.stream = _stream_handle(stream)
     h = device_graph(g)
+    if app.aggregator == "store":
+        return _run_store(g, app, a, cfg, h, mode, lane_width, shard, order, reduce)
     res = _native.WmResult()
     hist = None
     if app.aggregator == "pattern":
@@ -281,6 +287,85 @@ def run(g: CsrGraph, app: Application, *, mode: str = "wc", warps: int = None,
         extra={"bucket_words": res.bucket_words, "nodes": int(res.nodes),
                "polls": int(res.polls), "build_ms": res.build_ms,
                "h2d_bytes": int(res.h2d_bytes), "d2h_bytes": int(res.d2h_bytes)})
+    if reduce and shard[1] > 1:
+        from . import parallel
+        out = parallel.allreduce_result(out)
+    return out
+
+
+def _result(app, mode, lane_width, res, wall, shard, order, **kw) -> RunResult:
+    extra = {"bucket_words": res.bucket_words, "nodes": int(res.nodes),
+             "polls": int(res.polls), "build_ms": res.build_ms,
+             "h2d_bytes": int(res.h2d_bytes), "d2h_bytes": int(res.d2h_bytes)}
+    extra.update(kw.pop("extra", {}))
+    return RunResult(
+        app=app.name, k=app.k, mode=mode, warps=res.warps, lane_width=lane_width,
+        clique_count=kw.get("clique_count"), pattern_counts=kw.get("pattern_counts"),
+        records_emitted=kw.get("records_emitted"), aggregated_total=int(res.leaves),
+        ledgers=[], makespan_ticks=0, wall_seconds=wall,
+        rebalance_count=int(res.rebalance_count), migrations=int(res.migrations),
+        peak_extension_storage=int(res.peak_ext), kernel_ms=res.kernel_ms,
+        device_ms=res.device_ms, alg_bytes=int(res.alg_bytes),
+        idle_warp_fraction=res.idle_warp_fraction,
+        idle_warp_fraction_tail=res.idle_warp_fraction_tail, tasks=int(res.tasks),
+        launches=int(res.launches), devices=shard[1], order=order, extra=extra)
+
+
+def _run_store(g, app, a, cfg, h, mode, lane_width, shard, order, reduce) -> RunResult:
+    """listing_app through ``wm_run_listing``: device warps stream records
+    into a mapped ring (aggregate_store, reference ``aggregate.py:199-223``);
+    the native drain loop hands batches to ``sink`` below, which rebuilds
+    ``(vertices, bits)`` (traversal order, ``extend_bits``), applies the
+    predicate and ``put``s into the app's StoreBuffer — blocking there blocks
+    the device producers."""
+    from .apps import complete_subgraph
+    from .canon import group_offset
+    k = app.k
+    pred = app.store_predicate
+    lst = _native.WmListing()
+    lst.capacity = LISTING_RING
+    # the reference's complete_subgraph predicate runs on the device
+    lst.filter = _native.WM_LIST_COMPLETE if pred is complete_subgraph else _native.WM_LIST_ALL
+    host_pred = None if pred is complete_subgraph else pred
+    off = group_offset(k - 1) if k > 2 else 0
+    state = {"emitted": 0, "error": None}
+    store = app.store
+
+    def sink(user, recs, count, stride):
+        try:
+            rows = np.ctypeslib.as_array(recs, shape=(int(count) * int(stride),))
+            rows = rows.reshape(int(count), int(stride)).tolist()
+            for r in rows:
+                vertices = tuple(r[5:4 + k]) + (r[1],)
+                bits = r[3] | (r[4] << 32) | (r[2] << off)
+                if host_pred is not None and not host_pred(vertices, bits):
+                    continue
+                store.put((vertices, bits))
+                state["emitted"] += 1
+            return 0
+        except BaseException as exc:  # surfaced after the device stops
+            state["error"] = exc
+            return 1
+
+    native_only = store is NATIVE_STORE
+    if native_only:
+        if pred is not None and pred is not complete_subgraph:
+            raise ValueError("a Python predicate needs a Python store")
+        lst.sink = _native.SINK_FN()
+    else:
+        lst.sink = _native.SINK_FN(sink)
+    res = _native.WmResult()
+    t0 = time.perf_counter()
+    st = _native.load().wm_run_listing(h, ctypes.byref(a), ctypes.byref(cfg), ctypes.byref(lst),
+                                       ctypes.byref(res))
+    wall = time.perf_counter() - t0
+    if state["error"] is not None:
+        raise state["error"]
+    _native.check(st)
+    emitted = int(lst.emitted) if native_only else state["emitted"]
+    out = _result(app, mode, lane_width, res, wall, shard, order, records_emitted=emitted,
+                  extra={"checksum": int(lst.checksum), "records_streamed": int(lst.emitted),
+                         "stride_words": int(lst.stride_words)})
     if reduce and shard[1] > 1:
         from . import parallel
         out = parallel.allreduce_result(out)

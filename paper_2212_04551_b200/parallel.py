@@ -36,10 +36,17 @@ def shard_tasks(tasks, rank: int, count: int):
     return list(tasks)[rank::count]
 
 
+def _i64(x: int) -> int:
+    """u64 -> two's-complement int64 (sums stay exact mod 2^64)."""
+    x &= (1 << 64) - 1
+    return x - (1 << 64) if x >= 1 << 63 else x
+
+
 def pack(res) -> list:
     hist = res.pattern_counts or []
     return [res.clique_count or 0, res.aggregated_total, res.alg_bytes, res.migrations,
-            res.rebalance_count, res.tasks] + list(hist)
+            res.rebalance_count, res.tasks, res.records_emitted or 0,
+            _i64(res.extra.get("checksum", 0))] + list(hist)
 
 
 def allreduce_result(res, group=None, device=None):
@@ -62,11 +69,16 @@ def allreduce_result(res, group=None, device=None):
     dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
     v = [int(x) for x in vals.tolist()]
     tt = t.tolist()
+    extra = dict(res.extra)
+    if "checksum" in extra:
+        extra["checksum"] = v[7] & ((1 << 64) - 1)
     return replace(res,
                    clique_count=v[0] if res.clique_count is not None else None,
                    aggregated_total=v[1], alg_bytes=v[2], migrations=v[3],
                    rebalance_count=v[4], tasks=v[5],
-                   pattern_counts=v[6:] if res.pattern_counts is not None else None,
+                   records_emitted=v[6] if res.records_emitted is not None else None,
+                   pattern_counts=v[8:] if res.pattern_counts is not None else None,
+                   extra=extra,
                    kernel_ms=tt[0], device_ms=tt[1], wall_seconds=tt[2],
                    idle_warp_fraction=tt[3], idle_warp_fraction_tail=tt[4],
                    devices=dist.get_world_size(group))
