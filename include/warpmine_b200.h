@@ -51,6 +51,7 @@ extern "C" {
 
 #define WM_MODE_WC 1  /* warp-centric, load balancing off  (engine.py:18-19) */
 #define WM_MODE_OPT 2 /* warp-centric + on-device balancer (engine.py:20-21) */
+#define WM_MODE_DFS 3 /* thread-per-traversal DFS ablation, DM_DFS (engine.py:13-16) */
 
 #define WM_ORDER_ID 0     /* clique orientation by vertex id (reference order) */
 #define WM_ORDER_DEGREE 1 /* clique orientation by (degree, id) */
@@ -79,7 +80,7 @@ typedef struct {
 /* Run configuration: mode / balance_config (balance.py:36-60) plus the
  * B200-only knobs (root range, sharding, orientation, instrumentation). */
 typedef struct {
-  int mode;                 /* WM_MODE_WC | WM_MODE_OPT */
+  int mode;                 /* WM_MODE_WC | WM_MODE_OPT | WM_MODE_DFS */
   double lb_threshold;      /* donate when active/total warps < threshold
                                (balance.py:63-66); (0, 1] */
   int lb_poll;              /* DFS steps between idle-warp polls (>= 1) */

@@ -20,7 +20,7 @@ WM_OK, WM_EINVAL, WM_ECAPACITY, WM_EINVARIANT, WM_ECUDA, WM_ESHUTDOWN = 0, -1, -
 WM_F_LOWER, WM_F_COMPACT, WM_F_CLIQUE, WM_F_CANONICAL = 1, 2, 4, 8
 WM_AGG_COUNTER, WM_AGG_PATTERN, WM_AGG_STORE = 0, 1, 2
 WM_LIST_ALL, WM_LIST_COMPLETE = 0, 1
-WM_MODE_WC, WM_MODE_OPT = 1, 2
+WM_MODE_WC, WM_MODE_OPT, WM_MODE_DFS = 1, 2, 3
 WM_ORDER_ID, WM_ORDER_DEGREE = 0, 1
 
 EXPORTED = ("wm_graph_create", "wm_graph_create_device", "wm_run", "wm_run_listing",

@@ -275,8 +275,10 @@ void wm_graph_destroy(void *gp) {
 // engine.py:791-798 / balance.py:48-52, shared by wm_run and wm_run_listing
 static int check_run_args(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
   if (!g || !app || !cfg || !res) return fail(WM_EINVAL, "null argument");
-  if (cfg->mode != WM_MODE_WC && cfg->mode != WM_MODE_OPT)
-    return fail(WM_EINVAL, "mode must be wc or opt (dfs has no device path)");
+  if (cfg->mode != WM_MODE_WC && cfg->mode != WM_MODE_OPT && cfg->mode != WM_MODE_DFS)
+    return fail(WM_EINVAL, "mode must be one of dfs, wc, opt");
+  if (cfg->mode == WM_MODE_DFS && cfg->count_bytes)
+    return fail(WM_EINVAL, "count_bytes is measured on the warp-centric tree (wc/opt)");
   if (cfg->mode == WM_MODE_OPT && !(cfg->lb_threshold > 0.0 && cfg->lb_threshold <= 1.0))
     return fail(WM_EINVAL, "threshold must be in (0, 1]");
   if (cfg->mode == WM_MODE_OPT && cfg->lb_poll < 1)

@@ -616,6 +616,117 @@ __global__ void __launch_bounds__(256) clique_enum_kernel(CliqueArgs a) {
   warp_clock_end(a.L.lb, clk);
 }
 
+
+// --------------------------------------------------------------------------
+// 3) DM_DFS ablation (mode "dfs", reference engine.py:13-16, :274-294): one
+// THREAD per traversal, the paper's baseline that DFS-wide is measured
+// against (Table 4).  Each thread owns a root, keeps its candidate
+// lists C_L = C_{L-1} ∩ N+(tr[L-1]) in a private HBM arena and intersects
+// sorted lists by a scalar merge — uncoalesced, divergent, no warp
+// cooperation.  Same tree, same counts.
+
+// |a ∩ b| (both ascending), optionally writing the intersection to out
+__device__ __forceinline__ int merge_intersect(const int32_t *__restrict__ a, int na,
+                                               const int32_t *__restrict__ b, int nb,
+                                               int32_t *__restrict__ out) {
+  int i = 0, j = 0, c = 0;
+  while (i < na && j < nb) {
+    const int32_t x = a[i], y = __ldg(b + j);
+    if (x == y) {
+      if (out) out[c] = x;
+      ++c; ++i; ++j;
+    } else if (x < y) {
+      ++i;
+    } else {
+      ++j;
+    }
+  }
+  return c;
+}
+
+__global__ void __launch_bounds__(256) clique_dfs_kernel(
+    const int64_t *__restrict__ doff, const int32_t *__restrict__ dnbr,
+    const int32_t *__restrict__ tasks, unsigned long long ntasks, unsigned long long task_offset,
+    unsigned long long task_stride, int k, int32_t *__restrict__ arena, int cap,
+    unsigned long long *__restrict__ counters) {
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  int32_t *base = arena + tid * (unsigned long long)(k - 2) * (unsigned long long)cap;
+  unsigned long long acc = 0, nodes = 0, done = 0;
+  const int32_t *ptr[kMaxK];
+  int len[kMaxK], pos[kMaxK];
+  for (;;) {
+    const unsigned long long ti = atomicAdd(&counters[16], 1ull);  // root cursor (engine.py:187)
+    if (ti >= ntasks) break;
+    ++done;
+    const int32_t root = __ldg(tasks + task_offset + ti * task_stride);
+    const int64_t rb = __ldg(doff + root);
+    ptr[1] = dnbr + rb;
+    len[1] = (int)(__ldg(doff + root + 1) - rb);
+    pos[1] = 0;
+    int L = 1;
+    while (L >= 1) {
+      if (pos[L] == len[L]) { --L; continue; }
+      const int32_t v = ptr[L][pos[L]++];
+      const int64_t vb = __ldg(doff + v);
+      const int vd = (int)(__ldg(doff + v + 1) - vb);
+      ++nodes;
+      if (L == k - 2) {
+        acc += (unsigned long long)merge_intersect(ptr[L], len[L], dnbr + vb, vd, nullptr);
+      } else {
+        int32_t *out = base + (size_t)(L - 1) * cap;
+        const int c = merge_intersect(ptr[L], len[L], dnbr + vb, vd, out);
+        if (c >= k - L - 1) {
+          ++L;
+          ptr[L] = out;
+          len[L] = c;
+          pos[L] = 0;
+        }
+      }
+    }
+  }
+  acc = warp_sum_u64(acc);
+  nodes = warp_sum_u64(nodes);
+  done = warp_sum_u64(done);
+  if ((threadIdx.x & 31) == 0) {
+    atomicAdd(&counters[0], acc);
+    atomicAdd(&counters[2], done);
+    atomicAdd(&counters[3], nodes);
+  }
+}
+
+static int run_clique_dfs(Graph *g, const wm_cfg *cfg, int k, unsigned long long ntask,
+                          int maxout, wm_result *res, cudaStream_t s, cudaEvent_t k0,
+                          cudaEvent_t k1) {
+  unsigned long long *ctr = g->ws->counters.as<unsigned long long>();
+  const unsigned long long ro = (unsigned long long)cfg->shard_rank;
+  const unsigned long long nt =
+      ntask > ro ? (ntask - ro + cfg->shard_count - 1) / cfg->shard_count : 0;
+  // private arenas: (k-2) levels of maxout entries per thread; thread count
+  // bounded by the memory budget (a scaled-down copy of the reference's
+  // per-lane TE, engine.py:83-152)
+  const int cap = maxout > 0 ? maxout : 1;
+  const unsigned long long per = (unsigned long long)(k - 2) * cap * sizeof(int32_t);
+  size_t free_b = 0, total_b = 0;
+  WM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const unsigned long long budget = (unsigned long long)(free_b * 0.5) + g->ws->arena.bytes;
+  unsigned long long threads = (unsigned long long)g->num_sms * 2048ull;
+  if (threads > nt) threads = nt > 0 ? nt : 1;
+  while (threads > 256 && threads * per > budget) threads >>= 1;
+  const int blocks = (int)((threads + 255) / 256);
+  int st = g->ws->arena.ensure((size_t)blocks * 256 * per);
+  if (st) return st;
+  WM_CUDA(cudaEventRecord(k0, s));
+  if (nt)
+    clique_dfs_kernel<<<blocks, 256, 0, s>>>(
+        g->ws->dag_off.as<int64_t>(), g->ws->dag_nbr.as<int32_t>(), g->ws->vals_out.as<int32_t>(),
+        nt, ro, (unsigned long long)cfg->shard_count, k, g->ws->arena.as<int32_t>(), cap, ctr);
+  WM_CUDA(cudaGetLastError());
+  WM_CUDA(cudaEventRecord(k1, s));
+  res->warps = blocks * 8;
+  res->launches += nt ? 1 : 0;
+  return WM_OK;
+}
+
 // --------------------------------------------------------------------------
 // host launcher
 
@@ -743,6 +854,33 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   WM_CUDA(cudaMemcpyAsync(hb, ctr + 8, sizeof hb, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
   res->launches = 5;
+  if (cfg->mode == WM_MODE_DFS) {
+    unsigned long long ntask = 0;
+    for (int c = 0; c < 7; ++c) ntask += hb[c];
+    uint32_t key0 = 0;
+    if (ntask) {
+      WM_CUDA(cudaMemcpyAsync(&key0, g->ws->keys_out.ptr, sizeof key0, cudaMemcpyDeviceToHost, s));
+      WM_CUDA(cudaStreamSynchronize(s));
+    }
+    WM_CUDA(cudaMemsetAsync(ctr + 16, 0, sizeof(unsigned long long), s));
+    int st2 = run_clique_dfs(g, cfg, k, ntask, key0 ? (int)key0 - 1 : 1, res, s, kb, k1);
+    if (st2) return st2;
+    unsigned long long hc[8];
+    WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaEventRecord(e1, s));
+    WM_CUDA(cudaStreamSynchronize(s));
+    float kms = 0, dms = 0;
+    WM_CUDA(cudaEventElapsedTime(&kms, kb, k1));
+    WM_CUDA(cudaEventElapsedTime(&dms, e0, e1));
+    res->clique_count = hc[0];
+    res->leaves = hc[0];
+    res->tasks = hc[2];
+    res->nodes = hc[3];
+    res->kernel_ms = kms;
+    res->device_ms = dms;
+    res->d2h_bytes = sizeof hb + sizeof key0 + sizeof hc;
+    return WM_OK;
+  }
   if (hb[6]) {
     return fail(WM_ECAPACITY,
                 "%llu root(s) have more than 1024 out-neighbours under this orientation "

@@ -599,6 +599,207 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
   }
 }
 
+
+// --------------------------------------------------------------------------
+// DM_DFS ablation (mode "dfs", reference engine.py:13-16, :274-294): one
+// THREAD per traversal running the same E-recurrence as the warp kernel with
+// scalar loops — no ballot compaction, no cooperative probes, per-leaf
+// histogram atomics.  Same tree, same histograms / records.
+
+// scalar record emission (one ticket per record)
+__device__ __forceinline__ bool emit_one(const MotifArgs &a, unsigned long long &tail_cache,
+                                         const int32_t *tr, unsigned long long bm, int32_t e,
+                                         uint32_t mask) {
+  const ListRing &R = a.ring;
+  const unsigned long long idx = atomicAdd(R.head, 1ull);
+  unsigned sl = 128;
+  while (idx + 1ull > tail_cache + R.cap_mask + 1ull) {
+    tail_cache = aref_sys_u64(R.ctl[0]).load(cuda::std::memory_order_relaxed);
+    if (idx + 1ull <= tail_cache + R.cap_mask + 1ull) break;
+    if (aref_sys_u64(R.ctl[1]).load(cuda::std::memory_order_relaxed) ||
+        ld_relaxed(&a.L.lb->error)) {
+      raise_error(a.L.lb, WM_ESHUTDOWN);
+      return false;
+    }
+    __nanosleep(sl);
+    if (sl < 8192) sl <<= 1;
+  }
+  uint32_t *slot = R.slots + (idx & R.cap_mask) * R.stride;
+  slot[1] = (uint32_t)e;
+  slot[2] = mask;
+  slot[3] = (uint32_t)bm;
+  slot[4] = (uint32_t)(bm >> 32);
+  for (int j = 0; j < a.k - 1; ++j) slot[5 + j] = (uint32_t)tr[j];
+  __threadfence_system();
+  aref_sys_u32(slot[0]).store((uint32_t)(idx + 1ull), cuda::std::memory_order_relaxed);
+  return true;
+}
+
+template <bool LIST>
+__global__ void __launch_bounds__(256) motif_dfs_kernel(MotifArgs a) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  unsigned long long *sh = reinterpret_cast<unsigned long long *>(smraw);
+  if (a.smem_hist) {
+    for (uint32_t i = threadIdx.x; i < a.pattern_count; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+  }
+  const unsigned long long tid = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
+  uint32_t *base = a.arena + tid * a.warp_stride;
+  const int k = a.k;
+  const int L = k - 2;  // leaf level: E_L holds the candidates of tr[0..k-1)
+  const int off = group_off(k - 1);
+  const bool complete_only = LIST && a.ring.filter == WM_LIST_COMPLETE;
+  int32_t tr[kMaxK];
+  long long tb[kMaxK], te[kMaxK];
+  unsigned long long bm[kMaxK];
+  uint32_t size[kMaxK], cur[kMaxK];
+  unsigned long long leaves = 0, emitted = 0, nodes = 0, done = 0, tail_cache = 0;
+  bool ok = true, bad = false;
+  while (ok) {
+    const unsigned long long ti = atomicAdd(&a.counters[16], 1ull);  // engine.py:187
+    if (ti >= a.ntasks) break;
+    ++done;
+    const int32_t r = __ldg(a.tasks + a.task_offset + ti * a.task_stride);
+    tr[0] = r;
+    tb[0] = __ldg(a.off + r);
+    te[0] = __ldg(a.off + r + 1);
+    bm[0] = 0;
+    uint32_t *l1 = level_ptr(a, base, 1);
+    uint32_t n1 = 0;
+    for (long long p = tb[0]; p < te[0]; ++p) {
+      const int32_t e = __ldg(a.nbr + p);
+      if (e > r) l1[n1++] = (uint32_t)e | (1u << a.vbits);
+    }
+    size[1] = cur[1] = n1;
+    int s = 1;
+    while (ok) {
+      if (cur[s] == 0) {
+        if (s == 1) break;
+        --s;
+        continue;
+      }
+      const uint32_t ent = level_ptr(a, base, s)[--cur[s]];
+      const int32_t x = (int32_t)(ent & a.vmask);
+      tr[s] = x;
+      tb[s] = __ldg(a.off + x);
+      te[s] = __ldg(a.off + x + 1);
+      bm[s] = (s == 1) ? 0ull
+                       : (bm[s - 1] | ((unsigned long long)(ent >> a.vbits) << group_off(s)));
+      ++nodes;
+      const uint32_t *src = level_ptr(a, base, s);
+      if (s == L) {
+        // leaves of tr[0..k-1): A part (E_L, mask gains bit L), B part (N(x))
+        for (uint32_t i = 0; i < size[s] && ok; ++i) {
+          const uint32_t en = src[i];
+          const int32_t e = (int32_t)(en & a.vmask);
+          if (e <= x) continue;
+          const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
+          const uint32_t mask =
+              (en >> a.vbits) | ((uint32_t)adj_probe(a.nbr, e, eb, ee, x, tb[s], te[s]) << L);
+          ++leaves;
+          if (LIST) {
+            if (!complete_only || (bm[L] == a.ring.full_prefix && mask == a.ring.full_mask)) {
+              ok = emit_one(a, tail_cache, tr, bm[L], e, mask);
+              ++emitted;
+            }
+          } else {
+            const uint32_t pid = __ldg(a.table + ((uint32_t)bm[L] | (mask << off)));
+            if (pid >= a.pattern_count) bad = true;
+            else if (a.smem_hist) atomicAdd(sh + pid, 1ull);
+            else atomicAdd(a.hist + pid, 1ull);
+          }
+        }
+        unsigned long long nb = 0;
+        for (long long p = tb[s]; p < te[s] && ok; ++p) {
+          const int32_t e = __ldg(a.nbr + p);
+          if (e <= r) continue;
+          const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
+          bool keep = true;
+          for (int j = 0; j < L && keep; ++j)
+            keep = !adj_probe(a.nbr, e, eb, ee, tr[j], tb[j], te[j]);
+          if (!keep) continue;
+          ++nb;
+          if (LIST && !complete_only) {
+            ok = emit_one(a, tail_cache, tr, bm[L], e, 1u << L);
+            ++emitted;
+          }
+        }
+        leaves += nb;
+        if (!LIST && nb) {
+          const uint32_t pid = __ldg(a.table + ((uint32_t)bm[L] | ((1u << L) << off)));
+          if (pid >= a.pattern_count) bad = true;
+          else if (a.smem_hist) atomicAdd(sh + pid, nb);
+          else atomicAdd(a.hist + pid, nb);
+        }
+        continue;
+      }
+      // E_{s+1} from E_s and x = tr[s]
+      uint32_t *dst = level_ptr(a, base, s + 1);
+      uint32_t n = 0;
+      for (uint32_t i = 0; i < size[s]; ++i) {
+        const uint32_t en = src[i];
+        const int32_t e = (int32_t)(en & a.vmask);
+        if (e <= x) continue;
+        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
+        dst[n++] = en | ((uint32_t)adj_probe(a.nbr, e, eb, ee, x, tb[s], te[s]) << (a.vbits + s));
+      }
+      for (long long p = tb[s]; p < te[s]; ++p) {
+        const int32_t e = __ldg(a.nbr + p);
+        if (e <= r) continue;
+        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
+        bool keep = true;
+        for (int j = 0; j < s && keep; ++j)
+          keep = !adj_probe(a.nbr, e, eb, ee, tr[j], tb[j], te[j]);
+        if (keep) dst[n++] = (uint32_t)e | (1u << (a.vbits + s));
+      }
+      ++s;
+      size[s] = cur[s] = n;
+    }
+  }
+  if (bad) raise_error(a.L.lb, WM_EINVARIANT);
+  leaves = warp_sum_u64(leaves);
+  emitted = warp_sum_u64(emitted);
+  nodes = warp_sum_u64(nodes);
+  done = warp_sum_u64(done);
+  if (lane_id() == 0) {
+    atomicAdd(&a.counters[0], leaves);
+    atomicAdd(&a.counters[2], done);
+    atomicAdd(&a.counters[3], nodes);
+    if (LIST) atomicAdd(&a.counters[6], emitted);
+  }
+  if (a.smem_hist) {
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < a.pattern_count; i += blockDim.x)
+      if (sh[i]) atomicAdd(a.hist + i, sh[i]);
+  }
+}
+
+template <bool LIST>
+static int launch_motif_dfs(Graph *g, MotifArgs a, cudaStream_t s, int *warps_out, bool launch) {
+  const size_t smem = a.smem_hist ? ((size_t)a.pattern_count * 8 + 15) / 16 * 16 : 0;
+  const unsigned long long per = a.warp_stride * sizeof(uint32_t);
+  size_t free_b = 0, total_b = 0;
+  WM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const unsigned long long budget = (unsigned long long)(free_b * 0.6) + g->ws->arena.bytes;
+  unsigned long long threads = (unsigned long long)g->num_sms * 2048ull;
+  if (threads > a.ntasks) threads = a.ntasks > 0 ? a.ntasks : 1;
+  while (threads > 256 && threads * per > budget) threads >>= 1;
+  const int blocks = (int)((threads + 255) / 256);
+  int st = g->ws->arena.ensure((size_t)blocks * 256 * per);
+  if (st) return st;
+  if (!launch) return WM_OK;
+  a.arena = g->ws->arena.as<uint32_t>();
+  WM_CUDA(cudaMemsetAsync(a.counters + 16, 0, sizeof(unsigned long long), s));
+  if ((st = lb_prepare(g, a.L.lb, 1, 1u, &a.L, s))) return st;  // error flag only
+  auto kern = motif_dfs_kernel<LIST>;
+  if (smem > 48 * 1024)
+    WM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<blocks, 256, smem, s>>>(a);
+  WM_CUDA(cudaGetLastError());
+  *warps_out = blocks * 8;
+  return WM_OK;
+}
+
 template <bool BYTES, bool LIST>
 static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s, int *warps_out,
                         bool launch) {
@@ -852,8 +1053,11 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
     a.smem_hist = 0;
   }
   int warps = 0;
+  const bool dfs = cfg->mode == WM_MODE_DFS;
 #define WM_LAUNCH(GO)                                                            \
-  (bytes ? launch_motif<true, false>(g, cfg, a, s, &warps, GO)                   \
+  (dfs ? (lst ? launch_motif_dfs<true>(g, a, s, &warps, GO)                      \
+              : launch_motif_dfs<false>(g, a, s, &warps, GO)) :                  \
+  bytes ? launch_motif<true, false>(g, cfg, a, s, &warps, GO)                    \
          : (lst ? launch_motif<false, true>(g, cfg, a, s, &warps, GO)            \
                 : launch_motif<false, false>(g, cfg, a, s, &warps, GO)))
   if (a.ntasks) {

@@ -232,14 +232,12 @@ def run(g: CsrGraph, app: Application, *, mode: str = "wc", warps: int = None,
         raise ValueError("need lane_width >= 1")
     if balance_config is not None and mode != "opt":
         raise ValueError("balance configuration only applies to opt mode")
-    if mode == "dfs":
-        raise ValueError("mode 'dfs' (thread-per-traversal ablation) has no B200 kernel; "
-                         "use 'wc' or 'opt'")
     if order not in ("degree", "id"):
         raise ValueError("order must be 'degree' or 'id'")
     a, keep_table = _app_struct(app)
     cfg = _native.WmCfg()
-    cfg.mode = _native.WM_MODE_OPT if mode == "opt" else _native.WM_MODE_WC
+    cfg.mode = {"dfs": _native.WM_MODE_DFS, "wc": _native.WM_MODE_WC,
+                "opt": _native.WM_MODE_OPT}[mode]
     bc = balance_config or bal.default_config(app.name)
     if mode == "opt" and not bc.enabled:
         cfg.mode = _native.WM_MODE_WC

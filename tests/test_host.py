@@ -203,7 +203,7 @@ def test_app_validation():
 
 def test_run_argument_errors_before_device():
     g = complete_graph(5)
-    for kw in ({"mode": "bogus"}, {"warps": 0}, {"lane_width": 0}, {"mode": "dfs"},
+    for kw in ({"mode": "bogus"}, {"warps": 0}, {"lane_width": 0},
                {"mode": "wc", "balance_config": BalanceConfig()}, {"order": "random"}):
         with pytest.raises(ValueError):
             run(g, clique_app(3), **kw)
