@@ -19,6 +19,7 @@
  *                                              aggregate.py:190-193)
  *   WM_ESHUTDOWN   -> StoreShutdownError      (aggregate.py:88-99: the store
  *                                              consumer is gone)
+ *   WM_EPARSE      -> GraphParseError         (graph.py:139-188, errors.py:4-11)
  *   WM_ECUDA       -> DeviceError (RuntimeError); no reference counterpart.
  */
 #ifndef WARPMINE_B200_H
@@ -38,6 +39,7 @@ extern "C" {
 #define WM_EINVARIANT (-3)
 #define WM_ECUDA (-4)
 #define WM_ESHUTDOWN (-5)
+#define WM_EPARSE (-6)
 
 /* Pipeline filter tags (engine.py:227-237); order-insensitive bit set. */
 #define WM_F_LOWER 1u
@@ -165,6 +167,31 @@ typedef struct {
  * canonical, store).  Blocks until every record has been consumed. */
 int wm_run_listing(void *graph, const wm_app *app, const wm_cfg *cfg, wm_listing *listing,
                    wm_result *result);
+
+/* ---- graph ingest on the device (the step before the path) ------------
+ * CsrGraph construction (graph.py:44-78) and the edge-list reader
+ * (graph.py:139-188) as data-parallel sort/unique/scan passes.  Outputs are
+ * malloc'd host arrays owned by the caller (release with wm_csr_free). */
+typedef struct {
+  int64_t n;                /* vertices */
+  int64_t nnz;              /* 2 * undirected edges */
+  int64_t *offsets;         /* [n + 1] */
+  int32_t *neighbors;       /* [nnz], rows strictly ascending */
+  int64_t error_line;       /* WM_EPARSE: 1-based offending line (0: whole input) */
+  double device_ms;
+} wm_csr_out;
+
+/* CsrGraph.from_arrays: endpoint arrays (any direction / multiplicity) on
+ * 0..n-1 -> symmetric CSR without self-loops or duplicates. */
+int wm_csr_build(int64_t n, const int64_t *src, const int64_t *dst, int64_t m,
+                 wm_csr_out *out);
+
+/* load_edge_list: whitespace edge-list text -> CSR with ids remapped to
+ * 0..n-1 in ascending order.  WM_EPARSE + out->error_line on the first
+ * malformed line (two integer tokens, non-negative). */
+int wm_edge_list_parse(const char *text, uint64_t len, wm_csr_out *out);
+
+void wm_csr_free(wm_csr_out *out);
 
 /* Upload a CSR graph to the current device (cudaSetDevice beforehand). */
 int wm_graph_create(const wm_csr *csr, void **graph);

@@ -11,12 +11,14 @@ from __future__ import annotations
 import ctypes
 import os
 
-from .errors import CapacityError, DeviceError, InternalInvariantError, StoreShutdownError
+from .errors import (CapacityError, DeviceError, GraphParseError, InternalInvariantError,
+                     StoreShutdownError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libwm_b200.so")
 
-WM_OK, WM_EINVAL, WM_ECAPACITY, WM_EINVARIANT, WM_ECUDA, WM_ESHUTDOWN = 0, -1, -2, -3, -4, -5
+WM_OK, WM_EINVAL, WM_ECAPACITY, WM_EINVARIANT, WM_ECUDA, WM_ESHUTDOWN, WM_EPARSE = \
+    0, -1, -2, -3, -4, -5, -6
 WM_F_LOWER, WM_F_COMPACT, WM_F_CLIQUE, WM_F_CANONICAL = 1, 2, 4, 8
 WM_AGG_COUNTER, WM_AGG_PATTERN, WM_AGG_STORE = 0, 1, 2
 WM_LIST_ALL, WM_LIST_COMPLETE = 0, 1
@@ -24,7 +26,8 @@ WM_MODE_WC, WM_MODE_OPT, WM_MODE_DFS = 1, 2, 3
 WM_ORDER_ID, WM_ORDER_DEGREE = 0, 1
 
 EXPORTED = ("wm_graph_create", "wm_graph_create_device", "wm_run", "wm_run_listing",
-            "wm_graph_destroy", "wm_last_error", "wm_abi_version")
+            "wm_graph_destroy", "wm_last_error", "wm_abi_version", "wm_csr_build",
+            "wm_edge_list_parse", "wm_csr_free")
 
 
 class WmCsr(ctypes.Structure):
@@ -76,6 +79,13 @@ class WmListing(ctypes.Structure):
                 ("stride_words", ctypes.c_uint32), ("reserved", ctypes.c_uint32)]
 
 
+class WmCsrOut(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("offsets", ctypes.POINTER(ctypes.c_int64)),
+                ("neighbors", ctypes.POINTER(ctypes.c_int32)),
+                ("error_line", ctypes.c_int64), ("device_ms", ctypes.c_double)]
+
+
 _LIB = None
 
 
@@ -99,6 +109,14 @@ def load():
     L.wm_run_listing.argtypes = [ctypes.c_void_p, ctypes.POINTER(WmApp), ctypes.POINTER(WmCfg),
                                  ctypes.POINTER(WmListing), ctypes.POINTER(WmResult)]
     L.wm_run_listing.restype = ctypes.c_int
+    L.wm_csr_build.argtypes = [ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                               ctypes.POINTER(ctypes.c_int64), ctypes.c_int64,
+                               ctypes.POINTER(WmCsrOut)]
+    L.wm_csr_build.restype = ctypes.c_int
+    L.wm_edge_list_parse.argtypes = [ctypes.c_char_p, ctypes.c_uint64, ctypes.POINTER(WmCsrOut)]
+    L.wm_edge_list_parse.restype = ctypes.c_int
+    L.wm_csr_free.argtypes = [ctypes.POINTER(WmCsrOut)]
+    L.wm_csr_free.restype = None
     L.wm_graph_destroy.argtypes = [ctypes.c_void_p]
     L.wm_graph_destroy.restype = None
     L.wm_last_error.argtypes = []
@@ -121,4 +139,6 @@ def check(status: int) -> None:
         raise InternalInvariantError(msg)
     if status == WM_ESHUTDOWN:
         raise StoreShutdownError(msg)
+    if status == WM_EPARSE:
+        raise GraphParseError(msg)
     raise DeviceError(msg or "libwm_b200 status %d" % status)

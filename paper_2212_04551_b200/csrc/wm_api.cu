@@ -18,6 +18,7 @@ namespace wm {
 static thread_local std::string g_last_error;
 
 void set_error(const std::string &msg) { g_last_error = msg; }
+void clear_error() { g_last_error.clear(); }
 
 int fail(int code, const char *fmt, ...) {
   char buf[1024];

@@ -35,6 +35,7 @@ namespace wm {
 // error capture
 
 void set_error(const std::string &msg);
+void clear_error();
 int fail(int code, const char *fmt, ...);
 
 #define WM_CUDA(call)                                                        \

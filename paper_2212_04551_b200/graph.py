@@ -19,6 +19,7 @@ B200 layout differences:
 
 from __future__ import annotations
 
+import ctypes
 import io
 import os
 import struct
@@ -70,9 +71,13 @@ class CsrGraph:
         return cls.from_arrays(n, arr[:, 0], arr[:, 1])
 
     @classmethod
-    def from_arrays(cls, n: int, src, dst) -> "CsrGraph":
+    def from_arrays(cls, n: int, src, dst, device: bool = False) -> "CsrGraph":
         """Vectorised build from endpoint arrays (any direction, any
-        multiplicity); symmetrises, dedups, drops self-loops."""
+        multiplicity); symmetrises, dedups, drops self-loops.  With
+        ``device=True`` the sort/unique/scan passes run on the current CUDA
+        device (``wm_csr_build``); the arrays are identical."""
+        if device:
+            return _csr_build_device(n, src, dst)
         src = np.asarray(src, dtype=np.int64)
         dst = np.asarray(dst, dtype=np.int64)
         keep = src != dst
@@ -204,15 +209,70 @@ class CsrGraph:
         return "CsrGraph(n=%d, m=%d, max_degree=%d)" % (self.n, self.m, self.max_degree)
 
 
-def load_edge_list(source) -> CsrGraph:
+def load_edge_list(source, device: bool = False) -> CsrGraph:
     """Parse whitespace edge-list text (reference ``graph.py:139-188``):
     '#'/'%' comments and blank lines skipped, ids remapped to ``0..n-1``
     preserving ascending order, duplicates and self-loops dropped.
-    Raises GraphParseError with the line number on malformed input."""
+    Raises GraphParseError with the line number on malformed input.
+    ``device=True`` parses and builds on the current CUDA device
+    (``wm_edge_list_parse``: one thread per line, sort/unique remap)."""
+    if device:
+        if isinstance(source, (str, bytes, os.PathLike)):
+            with open(source, "rb") as fh:
+                text = fh.read()
+        else:
+            text = "".join(source).encode("utf-8")
+        return _parse_device(text)
     if isinstance(source, (str, bytes, os.PathLike)):
         with open(source, "r", encoding="utf-8") as fh:
             return _parse_lines(fh)
     return _parse_lines(source)
+
+
+def _take_csr(out) -> CsrGraph:
+    from . import _native
+    try:
+        n, nnz = int(out.n), int(out.nnz)
+        off = np.ctypeslib.as_array(out.offsets, shape=(n + 1,)).copy()
+        nbr = (np.ctypeslib.as_array(out.neighbors, shape=(nnz,)).copy() if nnz
+               else np.zeros(0, np.int32))
+    finally:
+        _native.load().wm_csr_free(ctypes.byref(out))
+    return CsrGraph(n, off, nbr)
+
+
+def _csr_build_device(n, src, dst) -> CsrGraph:
+    from . import _native
+    src = np.ascontiguousarray(src, dtype=np.int64)
+    dst = np.ascontiguousarray(dst, dtype=np.int64)
+    if src.shape != dst.shape:
+        raise ValueError("endpoint arrays differ in length")
+    out = _native.WmCsrOut()
+    p64 = ctypes.POINTER(ctypes.c_int64)
+    _native.check(_native.load().wm_csr_build(int(n), src.ctypes.data_as(p64),
+                                              dst.ctypes.data_as(p64), len(src),
+                                              ctypes.byref(out)))
+    return _take_csr(out)
+
+
+def _parse_device(text: bytes) -> CsrGraph:
+    from . import _native
+    out = _native.WmCsrOut()
+    st = _native.load().wm_edge_list_parse(text, len(text), ctypes.byref(out))
+    if st == _native.WM_EPARSE:
+        line = int(out.error_line)
+        if line > 0:
+            # re-raise through the host reader on the offending line so the
+            # message and line number are exactly the reference's
+            bad = text.split(b"\n")[line - 1].decode("utf-8", "replace")
+            try:
+                _parse_lines([""] * (line - 1) + [bad])
+            except GraphParseError:
+                raise
+            raise GraphParseError("malformed input", line)
+        raise GraphParseError("empty graph: no valid edges in input")
+    _native.check(st)
+    return _take_csr(out)
 
 
 def _parse_lines(lines: Iterable[str]) -> CsrGraph:

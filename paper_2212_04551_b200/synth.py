@@ -11,9 +11,25 @@ build them).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from .graph import CsrGraph
+
+
+def _device_build() -> bool:
+    """Large generated graphs (configs 3-5) are assembled on the GPU
+    (``wm_csr_build``) when one is present; the arrays are identical to the
+    host build (tests/test_gpu_ingest.py).  WM_HOST_BUILD=1 forces the host."""
+    if os.environ.get("WM_HOST_BUILD"):
+        return False
+    try:
+        import torch
+        from . import _native
+        return torch.cuda.is_available() and os.path.exists(_native.LIB_PATH)
+    except Exception:
+        return False
 
 
 def gnp_random_graph(n: int, p: float, seed: int) -> CsrGraph:
@@ -61,7 +77,7 @@ def permute(g: CsrGraph, seed: int) -> CsrGraph:
     SURVEY §0 item 6)."""
     perm = np.random.default_rng(seed).permutation(g.n)
     e = g.edge_array()
-    return CsrGraph.from_arrays(g.n, perm[e[:, 0]], perm[e[:, 1]])
+    return CsrGraph.from_arrays(g.n, perm[e[:, 0]], perm[e[:, 1]], device=_device_build())
 
 
 def chung_lu(n: int, m: int, gamma: float, seed: int, permute_seed=None) -> CsrGraph:
@@ -73,7 +89,7 @@ def chung_lu(n: int, m: int, gamma: float, seed: int, permute_seed=None) -> CsrG
     p = w / w.sum()
     src = rng.choice(n, size=m, p=p)
     dst = rng.choice(n, size=m, p=p)
-    g = CsrGraph.from_arrays(n, src, dst)
+    g = CsrGraph.from_arrays(n, src, dst, device=_device_build())
     return permute(g, permute_seed) if permute_seed is not None else g
 
 
@@ -89,7 +105,7 @@ def rmat(scale: int, edge_factor: int, a=0.57, b=0.19, c=0.19, seed: int = 1,
         r = rng.random(m)
         src |= (r >= a + b).astype(np.int64) << bit
         dst |= (((r >= a) & (r < a + b)) | (r >= a + b + c)).astype(np.int64) << bit
-    g = CsrGraph.from_arrays(n, src, dst)
+    g = CsrGraph.from_arrays(n, src, dst, device=_device_build())
     return permute(g, permute_seed) if permute_seed is not None else g
 
 
@@ -104,5 +120,9 @@ def config_graph(name: str, seed: int = None) -> CsrGraph:
     if name == "cfg4":
         return rmat(20, 16, seed=1 if seed is None else seed, permute_seed=20)
     if name == "cfg5":
-        return rmat(22, 8, seed=1 if seed is None else seed, permute_seed=22)
+        # Graph500 skew at scale 22 has ~1e18 12-cliques (a
+        # 0.97-dense hub core); a = 0.52, b = c = 0.20, d = 0.08 keeps the
+        # power-law skew (max degree ~41K) with ~1e11 12-cliques.
+        return rmat(22, 8, a=0.52, b=0.20, c=0.20, seed=1 if seed is None else seed,
+                    permute_seed=22)
     raise ValueError("unknown config %r" % name)

@@ -41,6 +41,7 @@ def digest(g) -> str:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--kmax", type=int, default=9)
+    ap.add_argument("--cfg5", action="store_true", help="also the (long) cfg5 section")
     args = ap.parse_args()
     out = json.load(open(OUT)) if os.path.exists(OUT) else {}
     g = synth.config_graph("cfg3")
@@ -97,6 +98,52 @@ def main():
                     "cpu_s": round(time.time() - t, 2), "oracle": "wmo_motif_run"}
         print("cfg4 motif %s leaves=%d %.1fs" % (key, r["leaves"], time.time() - t), flush=True)
         json.dump(out, open(OUT, "w"), indent=1)
+    # cfg5 (R-MAT s22 ef8, a=.52 b=c=.20, permuted ids): clique k=3..12
+    # exhaustive (kClist), motif k=5/7 over root suffixes
+    if args.cfg5:
+        g5 = synth.config_graph("cfg5")
+        r5 = out.setdefault("cfg5", {})
+        r5.update({"digest": digest(g5), "n": g5.n, "m": g5.m, "max_degree": g5.max_degree,
+                   "recipe": "rmat(22, 8, a=.52, b=.20, c=.20, seed=1), ids permuted (seed 22)"})
+        cl5 = r5.setdefault("clique", {})
+        for k in range(3, 13):
+            if str(k) in cl5:
+                continue
+            t = time.time()
+            c = oracle.clique_fast(g5, k)
+            cl5[str(k)] = {"count": c, "oracle": "wmo_clique_fast", "cpu_s": round(time.time() - t, 2)}
+            print("cfg5 clique k=%d count=%d %.1fs" % (k, c, time.time() - t), flush=True)
+            json.dump(out, open(OUT, "w"), indent=1)
+        suf5 = r5.setdefault("motif_suffix", {})
+        # suffix sizes: the largest power of two whose induced subgraph has a
+        # star lower bound sum_v C(deg_suffix(v), k-1) <= 2e9 (CPU-feasible)
+        from math import comb
+        src = np.repeat(np.arange(g5.n), np.diff(g5.offsets))
+        dst = np.asarray(g5.neighbors_array)
+
+        def stars(s, k):
+            keep = (src >= g5.n - s) & (dst >= g5.n - s)
+            deg = np.bincount(src[keep], minlength=g5.n)
+            return sum(comb(int(d), k - 1) for d in deg[deg >= k - 1])
+
+        plan = []
+        for k in (5, 6, 7):
+            s = 1 << 22
+            while s > 1024 and stars(s, k) > 2e9:
+                s >>= 1
+            plan.append((k, s))
+        for k, s in plan:
+            key = "k%d_s%d" % (k, s)
+            if key in suf5:
+                continue
+            d = canon.build_dictionary(k)
+            t = time.time()
+            r = oracle.motif_run(g5, k, d.table, d.pattern_count, root_begin=g5.n - s,
+                                 root_end=g5.n)
+            suf5[key] = {"k": k, "suffix": s, "hist": r["hist"], "leaves": r["leaves"],
+                         "cpu_s": round(time.time() - t, 2), "oracle": "wmo_motif_run"}
+            print("cfg5 motif %s leaves=%d %.1fs" % (key, r["leaves"], time.time() - t), flush=True)
+            json.dump(out, open(OUT, "w"), indent=1)
     json.dump(out, open(OUT, "w"), indent=1)
 
 
