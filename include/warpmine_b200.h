@@ -77,6 +77,10 @@ typedef struct {
   const uint32_t *dict_table; /* host, [dict_len]; pattern aggregator only */
   uint64_t dict_len;
   uint32_t pattern_count;
+  const void *dict_device;  /* optional device-resident copy of the table (then
+                               dict_table may be NULL): u16 entries with
+                               SENTINEL 0xFFFF (pattern_count < 65535) or u32 */
+  uint32_t dict_device_bits; /* 16 or 32 */
 } wm_app;
 
 /* Run configuration: mode / balance_config (balance.py:36-60) plus the
@@ -192,6 +196,15 @@ int wm_csr_build(int64_t n, const int64_t *src, const int64_t *dst, int64_t m,
 int wm_edge_list_parse(const char *text, uint64_t len, wm_csr_out *out);
 
 void wm_csr_free(wm_csr_out *out);
+
+/* ---- pattern dictionary on the device --------------------------------
+ * build_dictionary (canon.py:315-343): table[b] = pattern id of every
+ * reachable k-vertex bitmap b (SENTINEL 0xFFFFFFFF otherwise), ids ascending
+ * with the canonical (minimum) bitmap, byte-identical to the reference.
+ * table_out holds 2^(k(k-1)/2-1) entries (2^27 at k = 8); bitmaps_out
+ * receives the canonical bitmaps (bitmaps_cap entries at most). */
+int wm_dictionary_build(int k, uint32_t *table_out, uint64_t *bitmaps_out, uint32_t bitmaps_cap,
+                        uint32_t *pattern_count);
 
 /* Upload a CSR graph to the current device (cudaSetDevice beforehand). */
 int wm_graph_create(const wm_csr *csr, void **graph);

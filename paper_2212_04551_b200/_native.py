@@ -27,7 +27,7 @@ WM_ORDER_ID, WM_ORDER_DEGREE = 0, 1
 
 EXPORTED = ("wm_graph_create", "wm_graph_create_device", "wm_run", "wm_run_listing",
             "wm_graph_destroy", "wm_last_error", "wm_abi_version", "wm_csr_build",
-            "wm_edge_list_parse", "wm_csr_free")
+            "wm_edge_list_parse", "wm_csr_free", "wm_dictionary_build")
 
 
 class WmCsr(ctypes.Structure):
@@ -40,7 +40,8 @@ class WmApp(ctypes.Structure):
     _fields_ = [("k", ctypes.c_int), ("extend_all", ctypes.c_int), ("genedges", ctypes.c_int),
                 ("aggregator", ctypes.c_int), ("filters", ctypes.c_uint32),
                 ("dict_table", ctypes.POINTER(ctypes.c_uint32)), ("dict_len", ctypes.c_uint64),
-                ("pattern_count", ctypes.c_uint32)]
+                ("pattern_count", ctypes.c_uint32), ("dict_device", ctypes.c_void_p),
+                ("dict_device_bits", ctypes.c_uint32)]
 
 
 class WmCfg(ctypes.Structure):
@@ -117,6 +118,10 @@ def load():
     L.wm_edge_list_parse.restype = ctypes.c_int
     L.wm_csr_free.argtypes = [ctypes.POINTER(WmCsrOut)]
     L.wm_csr_free.restype = None
+    L.wm_dictionary_build.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_uint32),
+                                      ctypes.POINTER(ctypes.c_uint64), ctypes.c_uint32,
+                                      ctypes.POINTER(ctypes.c_uint32)]
+    L.wm_dictionary_build.restype = ctypes.c_int
     L.wm_graph_destroy.argtypes = [ctypes.c_void_p]
     L.wm_graph_destroy.restype = None
     L.wm_last_error.argtypes = []

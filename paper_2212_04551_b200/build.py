@@ -16,7 +16,7 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 OUT = os.path.join(HERE, "libwm_b200.so")
-SOURCES = ["wm_api.cu", "wm_clique.cu", "wm_motif.cu", "wm_ingest.cu"]
+SOURCES = ["wm_api.cu", "wm_clique.cu", "wm_motif.cu", "wm_ingest.cu", "wm_dict.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3",

@@ -152,7 +152,7 @@ def is_canonical_candidate(tr: Sequence[int], u: int, g) -> bool:
 class CanonicalDictionary:
     """Bitmap -> pattern id table (reference ``canon.py:217-296``)."""
 
-    __slots__ = ("k", "table", "pattern_count", "canonical_bitmaps", "_fast")
+    __slots__ = ("k", "table", "pattern_count", "canonical_bitmaps", "_fast", "__weakref__")
 
     def __init__(self, k: int, table: np.ndarray, canonical_bitmaps: list):
         self.k = k
@@ -238,15 +238,40 @@ def _valid_bitmaps(k: int) -> np.ndarray:
 _DICT_CACHE: dict = {}
 
 
-def build_dictionary(k: int, allow_large: bool = False) -> CanonicalDictionary:
+def _build_on_device(k: int) -> CanonicalDictionary:
+    """The orbit sweep on the GPU (``wm_dictionary_build``, csrc/wm_dict.cu)."""
+    import ctypes
+    from . import _native
+    table = np.empty(1 << stored_bits(k), dtype=np.uint32)
+    reps = np.zeros(1 << 16, dtype=np.uint64)
+    count = ctypes.c_uint32()
+    _native.check(_native.load().wm_dictionary_build(
+        k, table.ctypes.data_as(ctypes.POINTER(ctypes.c_uint32)),
+        reps.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64)), len(reps), ctypes.byref(count)))
+    return CanonicalDictionary(k, table, [int(b) for b in reps[:count.value]])
+
+
+def build_dictionary(k: int, allow_large: bool = False, device=None) -> CanonicalDictionary:
     """Full pattern dictionary for size ``k`` (reference ``canon.py:315-343``).
-    Deterministic; cached per process."""
+    Deterministic; cached per process.  ``device=True`` runs the orbit sweep
+    on the GPU (same bytes); ``None`` picks the GPU for k = 8, where the host
+    sweep over ~1e8 bitmaps is impractical."""
     if not 3 <= k <= K_MAX_LARGE:
         raise ValueError("dictionary supports 3 <= k <= %d, got k=%d" % (K_MAX_LARGE, k))
     if k > K_MAX_DEFAULT and not allow_large:
         raise ValueError("k=%d needs allow_large=True (2^%d-entry table)" % (k, stored_bits(k)))
-    if k in _DICT_CACHE:
+    if k in _DICT_CACHE and not device:
         d = _DICT_CACHE[k]
+        return CanonicalDictionary(k, d.table.copy(), d.canonical_bitmaps)
+    if device is None and k > K_MAX_DEFAULT:
+        try:
+            import torch
+            device = torch.cuda.is_available()
+        except ImportError:
+            device = False
+    if device:
+        d = _build_on_device(k)
+        _DICT_CACHE.setdefault(k, d)
         return CanonicalDictionary(k, d.table.copy(), d.canonical_bitmaps)
     table = np.full(1 << stored_bits(k), SENTINEL, dtype=np.uint32)
     reps: list = []

@@ -315,8 +315,10 @@ int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
   }
   if (motif) {
     if (app->k > 8) return fail(WM_EINVAL, "k must be in [3, 8], got %d", app->k);
-    if (!app->dict_table || app->dict_len != (1ull << (app->k * (app->k - 1) / 2 - 1)) ||
-        app->pattern_count < 1)
+    if ((!app->dict_table && !app->dict_device) ||
+        app->dict_len != (1ull << (app->k * (app->k - 1) / 2 - 1)) || app->pattern_count < 1 ||
+        (app->dict_device && app->dict_device_bits != 16 && app->dict_device_bits != 32) ||
+        (app->dict_device && app->dict_device_bits == 16 && app->pattern_count >= 0xFFFFu))
       return fail(WM_EINVAL, "pattern aggregation requires the k=%d dictionary", app->k);
     if (!user_hist) return fail(WM_EINVAL, "pattern_counts buffer required");
     return run_motif(g, app, cfg, res, s);

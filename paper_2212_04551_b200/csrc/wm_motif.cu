@@ -83,7 +83,8 @@ struct MotifArgs {
   int k;
   int vbits;
   uint32_t vmask;
-  const uint32_t *table;
+  const uint32_t *table;            // u32 dictionary, or
+  const uint16_t *table16;          // u16 dictionary (SENTINEL 0xFFFF)
   uint32_t pattern_count;
   uint32_t *arena;
   unsigned long long warp_stride;  // arena words per warp
@@ -196,6 +197,11 @@ __device__ __forceinline__ uint32_t build_next(const MotifArgs &a, MotifWarp &w,
   return cnt;
 }
 
+// dictionary lookup (aggregate.py:189); SENTINEL >= pattern_count either way
+__device__ __forceinline__ uint32_t dict_lookup(const MotifArgs &a, uint32_t bits) {
+  return a.table16 ? (uint32_t)__ldg(a.table16 + bits) : __ldg(a.table + bits);
+}
+
 // bump hist[pid] by the number of lanes sharing pid (lanes with valid)
 __device__ __forceinline__ void hist_add(const MotifArgs &a, unsigned long long *sh, bool valid,
                                          uint32_t pid) {
@@ -234,7 +240,7 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
         const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
         const uint32_t mask =
             (ent >> a.vbits) | ((uint32_t)adj_probe(a.nbr, e, eb, ee, x, xb, xe) << L);
-        pid = __ldg(a.table + (bits | (mask << off)));
+        pid = dict_lookup(a, bits | (mask << off));
         valid = true;
         bad |= pid >= a.pattern_count;
       }
@@ -258,7 +264,7 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     nb += __popc(__ballot_sync(0xffffffffu, keep));
   }
   if (nb) {
-    const uint32_t pid = __ldg(a.table + (bits | ((1u << L) << off)));
+    const uint32_t pid = dict_lookup(a, bits | ((1u << L) << off));
     if (pid >= a.pattern_count) bad = true;
     else if (lane == 0) {
       if (a.smem_hist) atomicAdd(sh + pid, nb);
@@ -703,7 +709,7 @@ __global__ void __launch_bounds__(256) motif_dfs_kernel(MotifArgs a) {
               ++emitted;
             }
           } else {
-            const uint32_t pid = __ldg(a.table + ((uint32_t)bm[L] | (mask << off)));
+            const uint32_t pid = dict_lookup(a, (uint32_t)bm[L] | (mask << off));
             if (pid >= a.pattern_count) bad = true;
             else if (a.smem_hist) atomicAdd(sh + pid, 1ull);
             else atomicAdd(a.hist + pid, 1ull);
@@ -726,7 +732,7 @@ __global__ void __launch_bounds__(256) motif_dfs_kernel(MotifArgs a) {
         }
         leaves += nb;
         if (!LIST && nb) {
-          const uint32_t pid = __ldg(a.table + ((uint32_t)bm[L] | ((1u << L) << off)));
+          const uint32_t pid = dict_lookup(a, (uint32_t)bm[L] | ((1u << L) << off));
           if (pid >= a.pattern_count) bad = true;
           else if (a.smem_hist) atomicAdd(sh + pid, nb);
           else atomicAdd(a.hist + pid, nb);
@@ -968,7 +974,8 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   if ((st = g->ws->vals_out.ensure(sizeof(int32_t) * n))) return st;
   if ((st = g->ws->counters.ensure(sizeof(unsigned long long) * 64))) return st;
   if ((st = g->ws->lb.ensure(sizeof(LbState) * 8))) return st;
-  if ((st = g->ws->table.ensure(sizeof(uint32_t) * app->dict_len))) return st;
+  const bool dict_dev = app->dict_device != nullptr;
+  if (!dict_dev && (st = g->ws->table.ensure(sizeof(uint32_t) * app->dict_len))) return st;
   if ((st = g->ws->hist.ensure(sizeof(unsigned long long) * app->pattern_count))) return st;
   size_t tmp_sort = 0;
   WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
@@ -983,8 +990,9 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   if (!lst) {
     WM_CUDA(cudaMemsetAsync(g->ws->hist.ptr, 0, sizeof(unsigned long long) * app->pattern_count,
                             s));
-    WM_CUDA(cudaMemcpyAsync(g->ws->table.ptr, app->dict_table, sizeof(uint32_t) * app->dict_len,
-                            cudaMemcpyHostToDevice, s));
+    if (!dict_dev)
+      WM_CUDA(cudaMemcpyAsync(g->ws->table.ptr, app->dict_table,
+                              sizeof(uint32_t) * app->dict_len, cudaMemcpyHostToDevice, s));
   }
   const int tpb = 256;
   const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
@@ -1014,7 +1022,11 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   a.k = k;
   a.vbits = vbits;
   a.vmask = (1u << vbits) - 1u;
-  a.table = g->ws->table.as<uint32_t>();
+  a.table = nullptr;
+  a.table16 = nullptr;
+  if (!dict_dev) a.table = g->ws->table.as<uint32_t>();
+  else if (app->dict_device_bits == 16) a.table16 = static_cast<const uint16_t *>(app->dict_device);
+  else a.table = static_cast<const uint32_t *>(app->dict_device);
   a.pattern_count = app->pattern_count;
   a.maxdeg = g->max_degree > 0 ? g->max_degree : 1;
   a.warp_stride = (unsigned long long)a.maxdeg * (unsigned long long)((k - 2) * (k - 1) / 2);
@@ -1089,7 +1101,7 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   float kms = 0, dms = 0;
   WM_CUDA(cudaEventElapsedTime(&kms, k0, k1));
   WM_CUDA(cudaEventElapsedTime(&dms, e0, e1));
-  res->h2d_bytes = lst ? 0 : sizeof(uint32_t) * app->dict_len;
+  res->h2d_bytes = (lst || dict_dev) ? 0 : sizeof(uint32_t) * app->dict_len;
   res->d2h_bytes = sizeof ntask + sizeof hc + sizeof hl +
                    (lst ? (uint64_t)lst->emitted * a.ring.stride * 4
                         : sizeof(unsigned long long) * app->pattern_count);

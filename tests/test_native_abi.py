@@ -47,7 +47,8 @@ def test_struct_layouts_match_header():
     src = open(os.path.join(ROOT, "include", "warpmine_b200.h")).read()
     src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
     for cname, py in (("wm_csr", _native.WmCsr), ("wm_app", _native.WmApp),
-                      ("wm_cfg", _native.WmCfg), ("wm_result", _native.WmResult)):
+                      ("wm_cfg", _native.WmCfg), ("wm_result", _native.WmResult),
+                      ("wm_listing", _native.WmListing), ("wm_csr_out", _native.WmCsrOut)):
         body = re.search(r"typedef struct \{([^{}]*)\}\s*" + cname + ";", src).group(1)
         fields = []
         for decl in body.split(";"):
@@ -66,6 +67,11 @@ def test_status_mapping():
     for code, exc in ((_native.WM_EINVAL, ValueError), (_native.WM_ECAPACITY, CapacityError),
                       (_native.WM_EINVARIANT, InternalInvariantError),
                       (_native.WM_ECUDA, DeviceError)):
+        with pytest.raises(exc):
+            _native.check(code)
+    from paper_2212_04551_b200.errors import GraphParseError, StoreShutdownError
+    for code, exc in ((_native.WM_ESHUTDOWN, StoreShutdownError),
+                      (_native.WM_EPARSE, GraphParseError)):
         with pytest.raises(exc):
             _native.check(code)
     _native.check(_native.WM_OK)
