@@ -15,7 +15,8 @@ from .errors import (CapacityError, DeviceError, GraphParseError, InternalInvari
                      StoreShutdownError)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libwm_b200.so")
+# WM_B200_LIB selects an alternative in-tree build (A/B kernel variants)
+LIB_PATH = os.environ.get("WM_B200_LIB") or os.path.join(_HERE, "libwm_b200.so")
 
 WM_OK, WM_EINVAL, WM_ECAPACITY, WM_EINVARIANT, WM_ECUDA, WM_ESHUTDOWN, WM_EPARSE = \
     0, -1, -2, -3, -4, -5, -6

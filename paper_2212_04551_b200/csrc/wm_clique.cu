@@ -238,6 +238,7 @@ template <int WMAX> struct CliqueSmem {
   uint32_t P[kMaxK * WMAX];            // unconsumed members       [s * w + x]
   unsigned long long below[kMaxK];     // leaves under the level's node (B_alg)
   int32_t last[kMaxK];                 // vertex appended at the level
+  uint32_t queue[64];                  // bulk4 pair ring: (i << 16) | j
 };
 
 struct CliqueArgs {
@@ -365,6 +366,52 @@ __device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const u
   return part;
 }
 
+
+#ifndef WM_BULK4_MINK
+#define WM_BULK4_MINK 5
+#endif
+
+// Four-level bulk for a node at traversal length k-4 with candidates C and
+// children to expand P: leaves = sum_{i in P} sum_{j in C_i} sum_{l in C_ij}
+// popc(C_ij & A[l]) with C_i = C & A[i], C_ij = C_i & A[j].  The (i, j)
+// pairs — the grandchildren, i.e. the (k-2)-cliques below the node — are
+// flattened through a 64-entry ring in shared memory so that all 32 lanes
+// take one pair each per round; bulk3's lane-per-j mapping leaves most
+// lanes idle once candidate sets are small (deep k).  Each lane then walks
+// the members l of its C_ij (the reference's last two extend/filter levels
+// done as one AND + popc per l).
+template <int w>
+__device__ __forceinline__ unsigned long long bulk4_round(const uint32_t *adj, const uint32_t (&c)[w],
+                                                          const uint32_t *queue, int head, int nq) {
+  constexpr int S = Width<w>::S;
+  const int lane = lane_id();
+  unsigned long long part = 0;
+  if (lane < nq) {
+    const uint32_t e = queue[(head + lane) & 63];
+    const int i = (int)(e >> 16), j = (int)(e & 0xffffu);
+    uint32_t ri[w], rj[w], cij[w];
+    load_row<w>(adj + i * S, ri);
+    load_row<w>(adj + j * S, rj);
+#pragma unroll
+    for (int x = 0; x < w; ++x) cij[x] = c[x] & ri[x] & rj[x];
+#pragma unroll
+    for (int y = 0; y < w; ++y) {
+      uint32_t m = cij[y];
+      while (m) {
+        const int l = y * 32 + __ffs(m) - 1;
+        m &= m - 1u;
+        uint32_t rl[w];
+        load_row<w>(adj + l * S, rl);
+        uint32_t t = 0;
+#pragma unroll
+        for (int x = 0; x < w; ++x) t += __popc(cij[x] & rl[x]);
+        part += t;
+      }
+    }
+  }
+  return part;
+}
+
 // Donate the upper half of the pending members of the shallowest level that
 // has any (reference balance.py:102-128 steals the shallowest pending entry;
 // one record here carries half of that level so a thief gets a large
@@ -431,14 +478,86 @@ struct TaskCounters {
   int poll;
 };
 
+// The pending children of a four-level bulk node stay in the stack's P[lv]
+// (popped one at a time, like move_step), so the balancer can donate half of
+// them mid-node: with whole bulk nodes as the unit of work the tail of a
+// small-k run would otherwise wait on the largest node.  Polls happen per
+// child, software-pipelined as in run_task.
+template <int w, int WMAX>
+__device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
+                                                    int lv, int s0, unsigned long long task,
+                                                    TaskCounters &tc, uint32_t &pt,
+                                                    uint32_t &ph) {
+  constexpr int S = Width<w>::S;
+  const int lane = lane_id();
+  const uint32_t *adj = sm.adj;
+  uint32_t *queue = sm.queue;
+  uint32_t *Ps = sm.P + lv * w;
+  uint32_t c[w];
+#pragma unroll
+  for (int x = 0; x < w; ++x) c[x] = sm.C[lv * w + x];
+  unsigned long long part = 0;
+  int head = 0, nq = 0;  // warp-uniform ring state
+  for (int q = 0; q < w; ++q) {
+    uint32_t pm = Ps[q];  // pending children of word q, in a register between polls
+    while (pm) {
+      const int i = q * 32 + __ffs(pm) - 1;
+      pm &= pm - 1u;
+      uint32_t ci[w];
+      load_row<w>(adj + i * S, ci);  // broadcast read
+#pragma unroll
+      for (int x = 0; x < w; ++x) {
+        const uint32_t word = ci[x] & c[x];  // the child's candidates: its own ballot
+        if ((word >> lane) & 1u)
+          queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] =
+              ((uint32_t)i << 16) | (uint32_t)(x * 32 + lane);
+        nq += __popc(word);
+        if (nq >= 32) {
+          __syncwarp();
+          part += bulk4_round<w>(adj, c, queue, head, 32);
+          __syncwarp();
+          head = (head + 32) & 63;
+          nq -= 32;
+        }
+      }
+      if (a.lb_on && ++tc.poll >= a.lb_poll) {
+        tc.poll = 0;
+        ++tc.polls;
+        int want = 0;
+        if (lane == 0) {
+          want = (int)(pt - ph) >= a.idle_min;
+          pt = (uint32_t)ld_relaxed(&a.L.lb->tail);
+          ph = (uint32_t)ld_relaxed(&a.L.lb->head);
+        }
+        if (__shfl_sync(0xffffffffu, want, 0)) {
+          // expose the pending children, donate, take back what is left
+          if (lane == 0) Ps[q] = pm;
+          __syncwarp();
+          try_donate<w>(sm.C, sm.P, a, s0, lv, task);
+          pm = Ps[q];
+          __syncwarp();
+        }
+      }
+    }
+    if (lane == 0) Ps[q] = 0u;
+  }
+  if (nq) {
+    __syncwarp();
+    part += bulk4_round<w>(adj, c, queue, head, nq);
+    __syncwarp();
+  }
+  return part;
+}
+
 // Process one task (root or donated level) of word width w.
 template <int w, int WMAX, bool BYTES>
 __device__ __noinline__ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
                                       unsigned long long task, int s0, int32_t root, int d,
                                       int64_t lb, const Rec3 &rec, bool stage,
-                                      TaskCounters &tc) {
+                                      TaskCounters &tcio) {
   constexpr int S = Width<w>::S;
   const int lane = lane_id();
+  TaskCounters tc = tcio;  // registers for the hot loop (tcio lives in local memory)
   const int k = a.k;
   uint32_t *C = sm.C;
   uint32_t *P = sm.P;
@@ -486,6 +605,19 @@ __device__ __noinline__ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
     sm.last[s0] = root;
   }
   __syncwarp();
+  // balancer poll, software-pipelined: the idle-ticket counters loaded at one
+  // poll are consumed at the next, so the L2 round trip never stalls the DFS
+  uint32_t pt = 0, ph = 0;  // low words suffice: tail - head is small
+  if (!BYTES && a.lb_on && lane == 0) {
+    pt = (uint32_t)ld_relaxed(&a.L.lb->tail);
+    ph = (uint32_t)ld_relaxed(&a.L.lb->head);
+  }
+  if (!BYTES && k >= WM_BULK4_MINK && s0 == k - 4) {
+    // the task itself is a four-level bulk node
+    tc.acc += bulk4<w, WMAX>(sm, a, s0, s0, task, tc, pt, ph);
+    tcio = tc;
+    return;
+  }
   if (s0 >= k - 3) {
     // the task itself is a bulk node
     unsigned long long bytes = 0;
@@ -497,6 +629,7 @@ __device__ __noinline__ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
       tc.bytes += bytes;
       if (warp_sum_u64(part) && lane == 0) tc.bytes += outdeg_bytes(a, root);
     }
+    tcio = tc;
     return;
   }
   int s = s0;
@@ -531,7 +664,11 @@ __device__ __noinline__ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
     __syncwarp();
     ++tc.nodes;
     if (cnt >= k - s - 1) {
-      if (s + 1 == k - 3) {
+      if (!BYTES && k >= WM_BULK4_MINK && s + 1 == k - 4) {
+        if (lane < w) P[(s + 1) * w + lane] = cw;
+        __syncwarp();
+        tc.acc += bulk4<w, WMAX>(sm, a, s + 1, s0, task, tc, pt, ph);
+      } else if (s + 1 == k - 3) {
         unsigned long long bytes = 0;
         const unsigned long long part =
             bulk3<w, BYTES>(adj, C + (s + 1) * w, C + (s + 1) * w, a, lb, bytes);
@@ -559,13 +696,25 @@ __device__ __noinline__ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
     if (!BYTES && a.lb_on && ++tc.poll >= a.lb_poll) {
       tc.poll = 0;
       ++tc.polls;
-      if (donation_wanted(a.L, a.idle_min)) try_donate<w>(C, P, a, s0, s, task);
+      int want = 0;
+      if (lane == 0) {
+        want = (int)(pt - ph) >= a.idle_min;
+        pt = (uint32_t)ld_relaxed(&a.L.lb->tail);
+        ph = (uint32_t)ld_relaxed(&a.L.lb->head);
+      }
+      if (__shfl_sync(0xffffffffu, want, 0)) try_donate<w>(C, P, a, s0, s, task);
     }
   }
+  tcio = tc;
 }
 
+// <= 51 registers for the narrow classes: 5 blocks (40 warps) per SM
+#ifndef WM_ENUM_MINBLOCKS
+#define WM_ENUM_MINBLOCKS 5
+#endif
 template <int WMAX, bool BYTES>
-__global__ void __launch_bounds__(256) clique_enum_kernel(CliqueArgs a) {
+__global__ void __launch_bounds__(256, WMAX <= 4 ? WM_ENUM_MINBLOCKS : 1)
+    clique_enum_kernel(CliqueArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   CliqueSmem<WMAX> &sm = reinterpret_cast<CliqueSmem<WMAX> *>(smraw)[threadIdx.x >> 5];
   const int lane = lane_id();
