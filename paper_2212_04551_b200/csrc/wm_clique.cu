@@ -239,6 +239,7 @@ template <int WMAX> struct CliqueSmem {
   unsigned long long below[kMaxK];     // leaves under the level's node (B_alg)
   int32_t last[kMaxK];                 // vertex appended at the level
   uint32_t queue[64];                  // bulk4 pair ring: (i << 16) | j
+  uint32_t crow[32];                   // bulk4 node compacted to <= 32 members
 };
 
 struct CliqueArgs {
@@ -370,6 +371,9 @@ __device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const u
 #ifndef WM_BULK4_MINK
 #define WM_BULK4_MINK 5
 #endif
+#ifndef WM_COMPACT_POLL_MIN
+#define WM_COMPACT_POLL_MIN 16
+#endif
 
 // Four-level bulk for a node at traversal length k-4 with candidates C and
 // children to expand P: leaves = sum_{i in P} sum_{j in C_i} sum_{l in C_ij}
@@ -478,6 +482,91 @@ struct TaskCounters {
   int poll;
 };
 
+// A wide (w > 1) four-level bulk node whose candidate set has m <= 32
+// members is first compacted to an m x m one-word bitmap (row r = members
+// above member r: one ballot per row), so the pair ring and the popc loop run
+// at w = 1 — a single AND + POPC per step instead of w of each.  For a
+// donation the pending compact children are mapped back to their original
+// bit positions in P[lv] (one OR-reduction per word) and re-read afterwards.
+template <int w, int WMAX>
+__device__ __forceinline__ unsigned long long bulk4_compact(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
+                                                            int lv, int m, int s0,
+                                                            unsigned long long task,
+                                                            TaskCounters &tc, uint32_t &pt,
+                                                            uint32_t &ph) {
+  const int lane = lane_id();
+  int pos = -1;  // this lane's member (original bit position)
+  {
+    int before = 0;
+#pragma unroll
+    for (int x = 0; x < w; ++x) {
+      const uint32_t cw = sm.C[lv * w + x];
+      const int cnt = __popc(cw);
+      if (pos < 0 && lane >= before && lane < before + cnt)
+        pos = x * 32 + (int)__fns(cw, 0, lane - before + 1);
+      before += cnt;
+    }
+  }
+  for (int r = 0; r < m; ++r) {
+    const int pr = __shfl_sync(0xffffffffu, pos, r);
+    const uint32_t *row = sm.adj + pr * w;
+    const bool bit = lane < m && ((row[pos >> 5] >> (pos & 31)) & 1u);
+    const unsigned bal = __ballot_sync(0xffffffffu, bit);
+    if (lane == 0) sm.crow[r] = bal;
+  }
+  uint32_t pc = __ballot_sync(0xffffffffu, lane < m && ((sm.P[lv * w + (pos >> 5)] >> (pos & 31)) & 1u));
+  const uint32_t c1[1] = {m == 32 ? 0xffffffffu : ((1u << m) - 1u)};
+  // only nodes with many members carry enough work to be worth splitting
+  const bool pollable = a.lb_on && m >= WM_COMPACT_POLL_MIN;
+  __syncwarp();
+  unsigned long long part = 0;
+  int head = 0, nq = 0;
+  while (pc) {
+    const int i = __ffs(pc) - 1;
+    pc &= pc - 1u;
+    const uint32_t word = sm.crow[i];  // row i is already restricted to C
+    if ((word >> lane) & 1u)
+      sm.queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] = ((uint32_t)i << 16) | (uint32_t)lane;
+    nq += __popc(word);
+    if (nq >= 32) {
+      __syncwarp();
+      part += bulk4_round<1>(sm.crow, c1, sm.queue, head, 32);
+      __syncwarp();
+      head = (head + 32) & 63;
+      nq -= 32;
+    }
+    if (pollable && ++tc.poll >= a.lb_poll) {
+      tc.poll = 0;
+      ++tc.polls;
+      int want = 0;
+      if (lane == 0) {
+        want = (int)(pt - ph) >= a.idle_min;
+        pt = (uint32_t)ld_relaxed(&a.L.lb->tail);
+        ph = (uint32_t)ld_relaxed(&a.L.lb->head);
+      }
+      if (__shfl_sync(0xffffffffu, want, 0)) {
+        const bool mine = lane < m && ((pc >> lane) & 1u);
+#pragma unroll
+        for (int x = 0; x < w; ++x) {
+          const uint32_t v = __reduce_or_sync(0xffffffffu, (mine && (pos >> 5) == x) ? 1u << (pos & 31) : 0u);
+          if (lane == 0) sm.P[lv * w + x] = v;
+        }
+        __syncwarp();
+        try_donate<w>(sm.C, sm.P, a, s0, lv, task);
+        pc = __ballot_sync(0xffffffffu,
+                           lane < m && ((sm.P[lv * w + (pos >> 5)] >> (pos & 31)) & 1u));
+        __syncwarp();
+      }
+    }
+  }
+  if (nq) {
+    __syncwarp();
+    part += bulk4_round<1>(sm.crow, c1, sm.queue, head, nq);
+    __syncwarp();
+  }
+  return part;
+}
+
 // The pending children of a four-level bulk node stay in the stack's P[lv]
 // (popped one at a time, like move_step), so the balancer can donate half of
 // them mid-node: with whole bulk nodes as the unit of work the tail of a
@@ -490,6 +579,12 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
                                                     uint32_t &ph) {
   constexpr int S = Width<w>::S;
   const int lane = lane_id();
+  if (w > 1) {
+    int m = 0;
+#pragma unroll
+    for (int x = 0; x < w; ++x) m += __popc(sm.C[lv * w + x]);
+    if (m <= 32) return bulk4_compact<w, WMAX>(sm, a, lv, m, s0, task, tc, pt, ph);
+  }
   const uint32_t *adj = sm.adj;
   uint32_t *queue = sm.queue;
   uint32_t *Ps = sm.P + lv * w;
@@ -508,6 +603,7 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
 #pragma unroll
       for (int x = 0; x < w; ++x) {
         const uint32_t word = ci[x] & c[x];  // the child's candidates: its own ballot
+        if (word == 0u) continue;
         if ((word >> lane) & 1u)
           queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] =
               ((uint32_t)i << 16) | (uint32_t)(x * 32 + lane);
