@@ -11,6 +11,7 @@ build them).
 
 from __future__ import annotations
 
+import functools
 import os
 
 import numpy as np
@@ -109,7 +110,10 @@ def rmat(scale: int, edge_factor: int, a=0.57, b=0.19, c=0.19, seed: int = 1,
     return permute(g, permute_seed) if permute_seed is not None else g
 
 
-# The benchmark configs of BASELINE.json.
+# The benchmark configs of BASELINE.json.  Graphs are
+# immutable, so one build per process is shared (configs 4-5 take ~10-60 s
+# of host RNG work).
+@functools.lru_cache(maxsize=4)
 def config_graph(name: str, seed: int = None) -> CsrGraph:
     if name == "cfg1":
         return gnp_random_graph(516, 1200 / 132870, 1 if seed is None else seed)

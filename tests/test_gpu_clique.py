@@ -133,3 +133,22 @@ def test_errors_map_to_reference_exceptions(cuda):
     with pytest.raises(ValueError):
         run(g, Application(name="x", k=3, extend_all=False, genedges=False,
                            pipeline=(("filter", lambda *a: True, ()),), aggregator="counter"))
+
+
+def test_cfg5_rmat_s22_clique_counts(scale_golden, cuda):
+    """Config 5 (R-MAT scale 22, ~33M edges): k-clique counts k=3..12 vs the
+    pinned restatement (kClist, tests/golden/make_golden_scale.py --cfg5)."""
+    import hashlib
+    import numpy as np
+    from paper_2212_04551_b200 import BalanceConfig, run_clique, synth
+    g = synth.config_graph("cfg5")
+    h = hashlib.sha256()
+    h.update(np.asarray(g.offsets, dtype="<i8").tobytes())
+    h.update(np.asarray(g.neighbors_array, dtype="<i4").tobytes())
+    assert h.hexdigest() == scale_golden["cfg5"]["digest"]
+    for k in range(3, 13):
+        want = scale_golden["cfg5"]["clique"][str(k)]["count"]
+        r = run_clique(g, k, mode="opt", balance_config=BalanceConfig(threshold=1.0))
+        assert r.clique_count == want, (k, r.clique_count, want)
+    r = run_clique(g, 6, mode="wc")
+    assert r.clique_count == scale_golden["cfg5"]["clique"]["6"]["count"]

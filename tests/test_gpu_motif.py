@@ -113,3 +113,16 @@ def test_root_suffix_and_shards(cuda):
         assert a == b
     parts = [run_motifs(g, 5, d, shard=(r, 3), reduce=False).pattern_counts for r in range(3)]
     assert [sum(x) for x in zip(*parts)] == full
+
+
+def test_cfg5_rmat_s22_root_suffix(scale_golden, cuda):
+    """Config 5 (R-MAT scale 22): k=5/6/7 motif histograms over root suffixes
+    (the induced subgraph on the last s ids) vs the pinned restatement."""
+    from paper_2212_04551_b200 import BalanceConfig, run_motifs, synth
+    g = synth.config_graph("cfg5")
+    for key, want in scale_golden["cfg5"]["motif_suffix"].items():
+        k, s = want["k"], want["suffix"]
+        for mode in ("wc", "opt"):
+            kw = {"balance_config": BalanceConfig(threshold=1.0)} if mode == "opt" else {}
+            r = run_motifs(g, k, dictionary(k), mode=mode, roots=(g.n - s, g.n), **kw)
+            assert r.pattern_counts == want["hist"], (key, mode)
