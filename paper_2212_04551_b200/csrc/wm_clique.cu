@@ -647,7 +647,12 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
 
 // Process one task (root or donated level) of word width w.
 template <int w, int WMAX, bool BYTES>
-__device__ __noinline__ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
+#ifdef WM_RUNTASK_INLINE
+__device__ __forceinline__
+#else
+__device__ __noinline__
+#endif
+void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
                                       unsigned long long task, int s0, int32_t root, int d,
                                       int64_t lb, const Rec3 &rec, bool stage,
                                       TaskCounters &tcio) {
