@@ -164,7 +164,10 @@ __device__ __forceinline__ void donate_record(const LbShared &L, const Rec3 &rec
   if (lane == 0) {
     // slot reuse guard: the record of ticket h - cap must have been consumed
     // (cap >= 8 x warps makes this wait practically never taken)
-    while (aref_u32(slot[0]).load(cuda::std::memory_order_acquire) != 0u) __nanosleep(64);
+    // relaxed polling: an acquire load per spin would invalidate the SM's L1
+    // (CCTL.IVALL) under the busy warps sharing it
+    while (aref_u32(slot[0]).load(cuda::std::memory_order_relaxed) != 0u) __nanosleep(64);
+    __threadfence();
   }
   __syncwarp();
 #pragma unroll
@@ -219,7 +222,9 @@ __device__ __forceinline__ int acquire_work(const LbShared &L, bool lb_on,
   for (;;) {
     int state = 0;  // 1 record, 2 exit
     if (lane == 0) {
-      if (aref_u32(slot[0]).load(cuda::std::memory_order_acquire) == (uint32_t)(t + 1)) state = 1;
+      // relaxed spin (no per-iteration L1 invalidation); the fence below
+      // orders the record reads after the observed sequence word
+      if (aref_u32(slot[0]).load(cuda::std::memory_order_relaxed) == (uint32_t)(t + 1)) state = 1;
       else if (ld_relaxed(&lb->active) <= 0 || ld_relaxed(&lb->error)) state = 2;
     }
     state = __shfl_sync(0xffffffffu, state, 0);
