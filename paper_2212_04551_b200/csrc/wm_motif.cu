@@ -121,6 +121,32 @@ __device__ __forceinline__ uint32_t *level_ptr(const MotifArgs &a, uint32_t *bas
   return base + (unsigned long long)a.maxdeg * (unsigned long long)((L - 1) * L / 2);
 }
 
+
+// Warp-cooperative lower bound: first position in the ascending CSR row
+// [b, e) holding a value > key.  Canonical candidates must exceed tr[0]
+// (canon.py:190-210), so row scans start there instead of filtering a hub's
+// whole row element by element.  32-ary search: <= 4 dependent loads for a
+// 64K-entry row.
+__device__ __forceinline__ long long row_first_above(const int32_t *__restrict__ nbr, long long b,
+                                                     long long e, int32_t key) {
+  const int lane = lane_id();
+  while (e - b > 32) {
+    const long long step = (e - b + 31) / 32;
+    const long long pos = b + step * lane;
+    const bool le = pos < e && __ldg(nbr + pos) <= key;
+    const unsigned bal = __ballot_sync(0xffffffffu, le);
+    const int cnt = __popc(bal);  // rows are ascending: the <= key prefix is lanes [0, cnt)
+    if (cnt == 0) return b;
+    const long long nb = b + step * (cnt - 1) + 1;
+    const long long ne = b + step * cnt;
+    b = nb;
+    e = ne < e ? ne : e;
+  }
+  const long long pos = b + lane;
+  const bool le = pos < e && __ldg(nbr + pos) <= key;
+  return b + __popc(__ballot_sync(0xffffffffu, le));
+}
+
 // warp-collective append with ballot+popc compaction
 __device__ __forceinline__ void emit(uint32_t *dst, uint32_t &cnt, bool keep, uint32_t val) {
   const int lane = lane_id();
@@ -135,7 +161,7 @@ __device__ __forceinline__ uint32_t build_first(const MotifArgs &a, MotifWarp &w
   uint32_t *dst = level_ptr(a, base, 1);
   const int32_t r = w.tr[0];
   uint32_t cnt = 0;
-  for (long long p0 = w.tb[0]; p0 < w.te[0]; p0 += 32) {
+  for (long long p0 = row_first_above(a.nbr, w.tb[0], w.te[0], r); p0 < w.te[0]; p0 += 32) {
     const long long p = p0 + lane;
     bool keep = false;
     uint32_t val = 0;
@@ -178,7 +204,7 @@ __device__ __forceinline__ uint32_t build_next(const MotifArgs &a, MotifWarp &w,
     emit(dst, cnt, keep, val);
   }
   // B part: neighbours of w new to the traversal's neighbourhood
-  for (long long p0 = xb; p0 < xe; p0 += 32) {
+  for (long long p0 = row_first_above(a.nbr, xb, xe, t0); p0 < xe; p0 += 32) {
     const long long p = p0 + lane;
     bool keep = false;
     uint32_t val = 0;
@@ -249,7 +275,7 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     hist_add(a, sh, valid && pid < a.pattern_count, pid);
   }
   unsigned long long nb = 0;
-  for (long long p0 = xb; p0 < xe; p0 += 32) {
+  for (long long p0 = row_first_above(a.nbr, xb, xe, t0); p0 < xe; p0 += 32) {
     const long long p = p0 + lane;
     bool keep = false;
     if (p < xe) {
@@ -386,7 +412,7 @@ __device__ __forceinline__ unsigned long long list_leaves(const MotifArgs &a, Mo
     ok = emit_records(a, w, keep, e, mask);
   }
   // B part (mask = 1 << L: e sees only tr[L], never complete for k >= 3)
-  for (long long p0 = xb; p0 < xe && ok; p0 += 32) {
+  for (long long p0 = row_first_above(a.nbr, xb, xe, t0); p0 < xe && ok; p0 += 32) {
     const long long p = p0 + lane;
     bool keep = false;
     int32_t e = 0;
