@@ -88,6 +88,60 @@ __global__ void orient_fill_kernel(int64_t n, const int64_t *__restrict__ off,
   }
 }
 
+
+// Edge-parallel orientation (the reference's filter_lower, engine.py:331-353,
+// applied once per edge): flag every directed edge (v, u) with u above v,
+// exclusive-scan the flags, scatter.  Rows stay ascending (the CSR is
+// row-major) and every hub row is spread over many threads instead of being
+// walked by one warp — the warp-per-vertex form spent 0.5 ms on cfg3, bound by
+// the 20K-entry hub rows' dependent loads.
+__global__ void orient_src_kernel(int64_t n, const int64_t *__restrict__ off,
+                                  int32_t *__restrict__ src) {
+  const int lane = lane_id();
+  for (int64_t v = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; v < n;
+       v += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    const int64_t b = off[v], e = off[v + 1];
+    for (int64_t p = b + lane; p < e; p += 32) src[p] = (int32_t)v;
+  }
+}
+
+__global__ void orient_flag_kernel(int64_t nnz, const int64_t *__restrict__ off,
+                                   const int32_t *__restrict__ nbr,
+                                   const int32_t *__restrict__ src, int order,
+                                   int32_t *__restrict__ flag) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p <= nnz;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    if (p == nnz) { flag[p] = 0; continue; }
+    const int32_t u = __ldg(nbr + p), v = __ldg(src + p);
+    int64_t du = 0, dv = 0;
+    if (order != WM_ORDER_ID) {
+      du = __ldg(off + u + 1) - __ldg(off + u);
+      dv = __ldg(off + v + 1) - __ldg(off + v);
+    }
+    flag[p] = above(order, du, u, dv, v) ? 1 : 0;
+  }
+}
+
+__global__ void orient_scatter_kernel(int64_t nnz, const int32_t *__restrict__ nbr,
+                                      const int32_t *__restrict__ flag,
+                                      const int32_t *__restrict__ pos,
+                                      int32_t *__restrict__ dnbr) {
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (int64_t)gridDim.x * blockDim.x)
+    if (flag[p]) dnbr[pos[p]] = __ldg(nbr + p);
+}
+
+__global__ void orient_off_kernel(int64_t n, const int64_t *__restrict__ off,
+                                  const int32_t *__restrict__ pos, int64_t *__restrict__ doff,
+                                  int32_t *__restrict__ outdeg) {
+  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v <= n;
+       v += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t a = pos[off[v]];
+    doff[v] = a;
+    outdeg[v] = v < n ? (int32_t)(pos[off[v + 1]] - a) : 0;
+  }
+}
+
 // sort keys: eligible roots (out-degree >= k-1, inside the root range) get
 // outdeg+1, others 0; values are vertex ids in ascending order so the stable
 // descending sort is deterministic (identical task lists on every rank).
@@ -1042,7 +1096,37 @@ static int launch_enum(Graph *g, const wm_cfg *cfg, CliqueArgs a, const EnumPlan
   return WM_OK;
 }
 
+// WM_PHASES=1: print per-phase device times of run_clique to stderr (tuning aid)
+struct PhaseTimer {
+  bool on = false;
+  cudaEvent_t ev[8];
+  const char *name[8];
+  int n = 0;
+  cudaStream_t s;
+  explicit PhaseTimer(cudaStream_t st) : s(st) {
+    const char *e = getenv("WM_PHASES");
+    on = e && *e == '1';
+  }
+  void mark(const char *nm) {
+    if (!on || n >= 8) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], s);
+    name[n++] = nm;
+  }
+  ~PhaseTimer() {
+    if (!on || n < 2) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int i = 1; i < n; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, "[wm phases] %-14s %8.3f ms\n", name[i], ms);
+    }
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+  }
+};
+
 int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s) {
+  PhaseTimer pt(s);
   const int64_t n = g->n;
   const int k = app->k;
   const int order = cfg->order == WM_ORDER_ID ? WM_ORDER_ID : WM_ORDER_DEGREE;
@@ -1060,7 +1144,13 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   if ((st = g->ws->table.ensure(sizeof(unsigned long long) * (n + 1)))) return st; // bm_off
   if ((st = g->ws->counters.ensure(sizeof(unsigned long long) * 64))) return st;
   if ((st = g->ws->lb.ensure(sizeof(LbState) * 8))) return st;
-  size_t tmp_scan = 0, tmp_sort = 0, tmp_scan2 = 0;
+  const int64_t nnz = g->nnz;
+  if ((st = g->ws->edge_src.ensure(sizeof(int32_t) * (nnz + 1)))) return st;
+  if ((st = g->ws->edge_flag.ensure(sizeof(int32_t) * (nnz + 1)))) return st;
+  if ((st = g->ws->edge_pos.ensure(sizeof(int32_t) * (nnz + 1)))) return st;
+  size_t tmp_scan = 0, tmp_sort = 0, tmp_scan2 = 0, tmp_scan3 = 0;
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan3, g->ws->edge_flag.as<int32_t>(),
+                                        g->ws->edge_pos.as<int32_t>(), (int)(nnz + 1), s));
   WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp_scan, g->ws->outdeg.as<int32_t>(),
                                         g->ws->dag_off.as<int64_t>(), (int)(n + 1), s));
   WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
@@ -1070,24 +1160,34 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
                                         g->ws->table.as<unsigned long long>(), (int)(n + 1), s));
   size_t tmp = tmp_scan > tmp_sort ? tmp_scan : tmp_sort;
   if (tmp_scan2 > tmp) tmp = tmp_scan2;
+  if (tmp_scan3 > tmp) tmp = tmp_scan3;
   if ((st = g->ws->cub_tmp.ensure(tmp))) return st;
 
   cudaEvent_t e0 = g->ws->ev[0], e1 = g->ws->ev[1], k0 = g->ws->ev[2], k1 = g->ws->ev[3], kb = g->ws->ev[4];
   WM_CUDA(cudaEventRecord(e0, s));
+  pt.mark("start");
   unsigned long long *ctr = g->ws->counters.as<unsigned long long>();
   WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
   const int tpb = 256;
   const int vblocks = (int)((n * 32 + tpb - 1) / tpb < (int64_t)g->num_sms * 64
                                 ? (n * 32 + tpb - 1) / tpb
                                 : (int64_t)g->num_sms * 64);
-  orient_count_kernel<<<vblocks, tpb, 0, s>>>(n, g->offsets, g->neighbors, order,
-                                              g->ws->outdeg.as<int32_t>());
-  WM_CUDA(cudaMemsetAsync(g->ws->outdeg.as<int32_t>() + n, 0, sizeof(int32_t), s));
+  const int pblocks = (int)((nnz + tpb) / tpb < (int64_t)g->num_sms * 32
+                                ? (nnz + tpb) / tpb
+                                : (int64_t)g->num_sms * 32);
+  const int nblocks = (int)((n + tpb) / tpb < (int64_t)g->num_sms * 16 ? (n + tpb) / tpb
+                                                                      : (int64_t)g->num_sms * 16);
+  int32_t *esrc = g->ws->edge_src.as<int32_t>(), *eflag = g->ws->edge_flag.as<int32_t>(),
+          *epos = g->ws->edge_pos.as<int32_t>();
+  orient_src_kernel<<<vblocks, tpb, 0, s>>>(n, g->offsets, esrc);
+  orient_flag_kernel<<<pblocks, tpb, 0, s>>>(nnz, g->offsets, g->neighbors, esrc, order, eflag);
   size_t tb = g->ws->cub_tmp.bytes;
-  WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, g->ws->outdeg.as<int32_t>(),
-                                        g->ws->dag_off.as<int64_t>(), (int)(n + 1), s));
-  orient_fill_kernel<<<vblocks, tpb, 0, s>>>(n, g->offsets, g->neighbors, order,
-                                             g->ws->dag_off.as<int64_t>(), g->ws->dag_nbr.as<int32_t>());
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, eflag, epos, (int)(nnz + 1), s));
+  orient_scatter_kernel<<<pblocks, tpb, 0, s>>>(nnz, g->neighbors, eflag, epos,
+                                                g->ws->dag_nbr.as<int32_t>());
+  orient_off_kernel<<<nblocks, tpb, 0, s>>>(n, g->offsets, epos, g->ws->dag_off.as<int64_t>(),
+                                            g->ws->outdeg.as<int32_t>());
+  pt.mark("orient");
   const int64_t rb = cfg->root_begin < 0 ? 0 : cfg->root_begin;
   const int64_t re = (cfg->root_end < 0 || cfg->root_end > n) ? n : cfg->root_end;
   const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
@@ -1100,6 +1200,7 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
       g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
       g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0, 32, s));
   bucket_count_kernel<<<eblocks, tpb, 0, s>>>(n, g->ws->keys_out.as<uint32_t>(), ctr + 8);
+  pt.mark("task sort");
   unsigned long long hb[8];
   WM_CUDA(cudaMemcpyAsync(hb, ctr + 8, sizeof hb, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
@@ -1194,10 +1295,14 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   int max_w = 0;
   double idle_w = 0, idle_tail_w = 0, tot_w = 0;
   int launched = 0;
+  pt.mark("plan+sync");
   WM_CUDA(cudaEventRecord(k0, s));
   // build all bitmaps, then enumerate
   for (int pass = 0; pass < 2; ++pass) {
-    if (pass == 1) WM_CUDA(cudaEventRecord(kb, s));
+    if (pass == 1) {
+      WM_CUDA(cudaEventRecord(kb, s));
+      pt.mark("bitmap build");
+    }
     unsigned long long begin = 0;
     for (int c = 5; c >= 0 && pass == 0; --c) {
       const unsigned long long cnt = hb[c];
@@ -1258,12 +1363,14 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
     }
   }
   WM_CUDA(cudaEventRecord(k1, s));
+  pt.mark("enumerate");
   unsigned long long hc[8];
   WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
   LbState hl[8];
   if (launched)
     WM_CUDA(cudaMemcpyAsync(hl, lbs, sizeof(LbState) * launched, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaEventRecord(e1, s));
+  pt.mark("readback");
   WM_CUDA(cudaStreamSynchronize(s));
   float kms = 0, dms = 0, bms = 0;
   WM_CUDA(cudaEventElapsedTime(&bms, k0, kb));
