@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
 // its own word count (1, 2 or 4) over a shared per-warp buffer, so small
 // roots pay for narrow rows only.
 
-template <int WMAX> struct CliqueSmem {
+template <int WMAX> struct alignas(16) CliqueSmem {  // 16B: uint4 row loads
   static constexpr int D = 32 * WMAX;
   static constexpr int S = WMAX;
   uint32_t adj[D * S];                 // local DAG rows, stride w (16B-aligned vector loads)
