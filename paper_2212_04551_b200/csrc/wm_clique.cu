@@ -549,18 +549,21 @@ __device__ __forceinline__ unsigned long long bulk4_compact(CliqueSmem<WMAX> &sm
                                                             TaskCounters &tc, uint32_t &pt,
                                                             uint32_t &ph) {
   const int lane = lane_id();
-  int pos = -1;  // this lane's member (original bit position)
+  // member r's original bit position, scattered by bit lanes (crow is
+  // scratch until the compact rows are written)
   {
     int before = 0;
 #pragma unroll
     for (int x = 0; x < w; ++x) {
       const uint32_t cw = sm.C[lv * w + x];
-      const int cnt = __popc(cw);
-      if (pos < 0 && lane >= before && lane < before + cnt)
-        pos = x * 32 + (int)__fns(cw, 0, lane - before + 1);
-      before += cnt;
+      if ((cw >> lane) & 1u)
+        sm.crow[before + __popc(cw & ((1u << lane) - 1u))] = (uint32_t)(x * 32 + lane);
+      before += __popc(cw);
     }
   }
+  __syncwarp();
+  const int pos = lane < m ? (int)sm.crow[lane] : -1;  // this lane's member
+  __syncwarp();
   for (int r = 0; r < m; ++r) {
     const int pr = __shfl_sync(0xffffffffu, pos, r);
     const uint32_t *row = sm.adj + pr * w;
