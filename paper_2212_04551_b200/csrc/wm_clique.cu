@@ -207,13 +207,17 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
                                                            const int32_t *__restrict__ tasks,
                                                            unsigned long long ntask,
                                                            const unsigned long long *__restrict__ bm_off,
-                                                           uint32_t *__restrict__ bm) {
+                                                           uint32_t *__restrict__ bm,
+                                                           unsigned long long first,
+                                                           unsigned long long stride) {
   extern __shared__ __align__(16) unsigned char smraw[];
   BuildSmem<W> &sm = reinterpret_cast<BuildSmem<W> *>(smraw)[threadIdx.x >> 5];
   const int lane = lane_id();
   const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-  for (unsigned long long t = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-       t < ntask; t += nwarps) {
+  // only this shard's tasks (first + j * stride) need a bitmap
+  for (unsigned long long t = first + stride * (((unsigned long long)blockIdx.x * blockDim.x +
+                                                 threadIdx.x) >> 5);
+       t < ntask; t += nwarps * stride) {
     const int32_t v = __ldg(tasks + t);
     const int64_t b = __ldg(doff + v);
     const int d = (int)(__ldg(doff + v + 1) - b);
@@ -1038,7 +1042,8 @@ static int run_clique_dfs(Graph *g, const wm_cfg *cfg, int k, unsigned long long
 // host launcher
 
 template <int W>
-static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask, cudaStream_t s) {
+static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask,
+                        unsigned long long first, unsigned long long stride, cudaStream_t s) {
   const size_t per_warp = sizeof(BuildSmem<W>);
   int wpb = 8;
   while (wpb > 1 && per_warp * wpb > 200 * 1024) wpb >>= 1;
@@ -1049,10 +1054,12 @@ static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask,
   WM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
   if (bps < 1) return fail(WM_ECAPACITY, "clique build kernel W=%d does not fit on an SM", W);
   unsigned long long blocks = (unsigned long long)g->num_sms * bps;
-  const unsigned long long need = (ntask + wpb - 1) / wpb;
+  const unsigned long long mine = first < ntask ? (ntask - first + stride - 1) / stride : 0;
+  if (!mine) return WM_OK;
+  const unsigned long long need = (mine + wpb - 1) / wpb;
   if (blocks > need) blocks = need;
   kern<<<(int)blocks, wpb * 32, smem, s>>>(a.doff, a.dnbr, a.tasks, ntask, a.bm_off,
-                                           const_cast<uint32_t *>(a.bm));
+                                           const_cast<uint32_t *>(a.bm), first, stride);
   WM_CUDA(cudaGetLastError());
   return WM_OK;
 }
@@ -1317,11 +1324,18 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
       a.bm_off = bm_off + begin;
       a.bm = g->ws->arena.as<uint32_t>();
       begin += cnt;
-      // every task of the bucket gets a bitmap so offsets stay shard-independent
+      // arena offsets cover every task (shard-independent); only this shard's
+      // tasks are built: class-local index (class_off + t) = rank (mod N)
+      unsigned long long class_off = 0;
+      for (int c2 = 2; c2 > c; --c2) class_off += hb[c2];  // buckets 0-2 share a class
+      if (c > 2) class_off = 0;
+      const unsigned long long N = (unsigned long long)cfg->shard_count;
+      const unsigned long long first =
+          ((unsigned long long)cfg->shard_rank + N - class_off % N) % N;
       switch (c) {
 #define WM_BCASE(CC, WW) \
   case CC:               \
-    st = launch_build<WW>(g, a, cnt, s); \
+    st = launch_build<WW>(g, a, cnt, first, N, s); \
     break;
         WM_BCASE(0, 1) WM_BCASE(1, 2) WM_BCASE(2, 4) WM_BCASE(3, 8) WM_BCASE(4, 16)
         WM_BCASE(5, 32)
