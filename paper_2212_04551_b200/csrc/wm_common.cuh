@@ -50,6 +50,9 @@ int fail(int code, const char *fmt, ...);
 // device helpers
 
 constexpr int kWarp = 32;
+#ifndef WM_INTERP_MIN
+#define WM_INTERP_MIN 16  // rows longer than this start with interpolation probes
+#endif
 constexpr int kMaxK = 12;
 constexpr int kSlotWords = 128;  // ring slot: [0] seq (ticket+1), [32..127] record
 
@@ -78,9 +81,32 @@ __device__ __forceinline__ int lower_bound_i(const T *a, int n, T x) {
   return lo;
 }
 
-// membership of x in the ascending CSR row [b, e) of nbr (global, read-only)
+// membership of x in the ascending CSR row [b, e) of nbr (global, read-only).
+// Long rows start with interpolation probes: ids are (randomly permuted)
+// vertex numbers, so a row is close to a uniform sample of [0, n) and each
+// probe shrinks the range to ~sqrt of itself — a 64K-entry hub row takes
+// ~5 dependent loads instead of 16.  Binary search finishes (and bounds the
+// cost on skewed rows).
 __device__ __forceinline__ bool row_contains(const int32_t *__restrict__ nbr, int64_t b,
                                              int64_t e, int32_t x) {
+  if (e - b > WM_INTERP_MIN) {
+    int64_t lo = b, hi = e - 1;
+    int32_t vlo = __ldg(nbr + lo), vhi = __ldg(nbr + hi);
+    if (x <= vlo) return x == vlo;
+    if (x >= vhi) return x == vhi;
+    // invariant: vlo < x < vhi, candidates strictly inside (lo, hi)
+#pragma unroll 1
+    for (int it = 0; it < 3 && hi - lo > 8; ++it) {
+      const float f = (float)(x - vlo) / (float)(vhi - vlo);
+      int64_t pos = lo + 1 + (int64_t)(f * (float)(hi - lo - 1));
+      pos = pos < lo + 1 ? lo + 1 : (pos > hi - 1 ? hi - 1 : pos);
+      const int32_t y = __ldg(nbr + pos);
+      if (y == x) return true;
+      if (y < x) { lo = pos; vlo = y; } else { hi = pos; vhi = y; }
+    }
+    b = lo + 1;
+    e = hi;
+  }
   while (b < e) {
     int64_t mid = (b + e) >> 1;
     int32_t y = __ldg(nbr + mid);
