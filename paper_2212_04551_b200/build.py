@@ -19,7 +19,7 @@ OUT = os.path.join(HERE, "libwm_b200.so")
 SOURCES = ["wm_api.cu", "wm_clique.cu", "wm_motif.cu", "wm_ingest.cu", "wm_dict.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
-FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-Xptxas", "-O3",
+FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fopenmp", "-Xptxas", "-O3",
                 "-I", os.path.join(ROOT, "include")]
 
 
@@ -63,7 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if todo or not os.path.exists(OUT) or any(os.path.getmtime(o) > os.path.getmtime(OUT)
                                               for o in objs):
         tmp = OUT + ".tmp"
-        _run([NVCC, *ARCH, "-shared", "-o", tmp, *objs], verbose)
+        _run([NVCC, *ARCH, "-shared", "-Xcompiler", "-fopenmp", "-o", tmp, *objs, "-lgomp"],
+             verbose)
         os.replace(tmp, OUT)
     return OUT
 

@@ -331,7 +331,7 @@ struct Workspace {
   cudaStream_t own_stream = nullptr;
   cudaMemPool_t pool = nullptr;  // stream-ordered pool for graph arrays
   DeviceBuffer dag_off, dag_nbr, outdeg, keys_in, keys_out, vals_in, vals_out, cub_tmp;
-  DeviceBuffer lb, ring, counters, hist, arena, table, listing;
+  DeviceBuffer lb, ring, counters, hist, arena, table, listing, listing_ring;
   DeviceBuffer edge_src, edge_flag, edge_pos;  // clique orientation, per directed edge
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };

@@ -59,14 +59,22 @@ __global__ void motif_task_keys_kernel(int64_t n, const int32_t *__restrict__ de
   }
 }
 
-// Listing ring (aggregate_store, aggregate.py:199-223): records go to mapped
-// pinned host memory; `head` (device) hands out record tickets, ctl[0] (host)
-// is the consumer's tail, ctl[1] its failure flag.  A producer blocks while
-// its ticket is more than `cap` ahead of the tail (StoreBuffer back-pressure,
-// aggregate.py:69-99).
+// Listing ring (aggregate_store, aggregate.py:199-223): records are staged in
+// an HBM ring; `head` (device) hands out record tickets; each block of
+// 2^block_shift tickets has a completion counter the producers bump after
+// their records are written (and fenced).  The host copies completed blocks
+// with the copy engine and publishes its tail with a small H2D copy into
+// device memory (ctl[0]; ctl[1] = consumer failed) — producers waiting for
+// space poll L2, never host memory (thousands of warps reading sysmem would
+// starve the very copies they wait for).  A producer blocks while its ticket is more than
+// `cap` ahead of the tail (StoreBuffer back-pressure, aggregate.py:69-99).
+// Small scattered stores straight into mapped host memory ran at ~1.4 GB/s
+// over PCIe; the HBM ring + bulk DMA runs at copy-engine speed.
 struct ListRing {
-  uint32_t *slots;                 // host-mapped [cap * stride]
-  unsigned long long *ctl;         // host-mapped [0] tail [1] failed
+  uint32_t *slots;                 // device [cap * stride]
+  uint32_t *blockdone;             // device [cap >> block_shift] records written per block
+  uint32_t block_shift;
+  unsigned long long *ctl;         // device [0] tail [1] failed (written by host DMA)
   unsigned long long *head;        // device ticket counter
   unsigned long long cap_mask;
   uint32_t stride;                 // words per record (k + 4)
@@ -330,9 +338,9 @@ __device__ __forceinline__ bool emit_records(const MotifArgs &a, MotifWarp &w, b
     const unsigned long long need = base + (unsigned long long)n;
     unsigned sl = 128;
     while (need > w.tail_cache + R.cap_mask + 1ull) {
-      w.tail_cache = aref_sys_u64(R.ctl[0]).load(cuda::std::memory_order_relaxed);
+      w.tail_cache = aref_u64(R.ctl[0]).load(cuda::std::memory_order_relaxed);
       if (need <= w.tail_cache + R.cap_mask + 1ull) break;
-      if (aref_sys_u64(R.ctl[1]).load(cuda::std::memory_order_relaxed) ||
+      if (aref_u64(R.ctl[1]).load(cuda::std::memory_order_relaxed) ||
           ld_relaxed(&a.L.lb->error)) {
         ok = 0;
         break;
@@ -348,29 +356,35 @@ __device__ __forceinline__ bool emit_records(const MotifArgs &a, MotifWarp &w, b
     return false;
   }
   __syncwarp();
-  // record payload, coalesced over the warp (word 0, the sequence, last)
+  // record payload, coalesced over the warp
   const uint32_t st = R.stride;
   const int nw = n * (int)st;
   const unsigned long long bm = w.bm[a.k - 2];
   for (int i = lane; i < nw; i += 32) {
     const int r = i / (int)st, j = i - r * (int)st;
-    if (j == 0) continue;
     uint32_t v;
-    if (j == 1) v = (uint32_t)w.le[r];
+    if (j == 0) v = (uint32_t)(base + (unsigned long long)r + 1ull);  // ticket + 1
+    else if (j == 1) v = (uint32_t)w.le[r];
     else if (j == 2) v = w.lm[r];
     else if (j == 3) v = (uint32_t)bm;
     else if (j == 4) v = (uint32_t)(bm >> 32);
     else v = (uint32_t)w.tr[j - 5];
     R.slots[((base + (unsigned long long)r) & R.cap_mask) * st + j] = v;
   }
-  __threadfence_system();
+  __threadfence();
   __syncwarp();
-  if (keep) {
-    const unsigned long long idx = base + (unsigned long long)rank;
-    aref_sys_u32(R.slots[(idx & R.cap_mask) * st])
-        .store((uint32_t)(idx + 1ull), cuda::std::memory_order_relaxed);
+  // completion counts per ring block (a warp's tickets span at most two)
+  if (lane == 0) {
+    const unsigned long long b0 = base >> R.block_shift, b1 = (base + n - 1) >> R.block_shift;
+    const uint32_t nblk = (uint32_t)(R.cap_mask >> R.block_shift);  // block count - 1
+    if (b0 == b1) {
+      atomicAdd(R.blockdone + (b0 & nblk), (uint32_t)n);
+    } else {
+      const uint32_t n0 = (uint32_t)((b1 << R.block_shift) - base);
+      atomicAdd(R.blockdone + (b0 & nblk), n0);
+      atomicAdd(R.blockdone + (b1 & nblk), (uint32_t)n - n0);
+    }
   }
-  __syncwarp();
   return true;
 }
 
@@ -646,9 +660,9 @@ __device__ __forceinline__ bool emit_one(const MotifArgs &a, unsigned long long 
   const unsigned long long idx = atomicAdd(R.head, 1ull);
   unsigned sl = 128;
   while (idx + 1ull > tail_cache + R.cap_mask + 1ull) {
-    tail_cache = aref_sys_u64(R.ctl[0]).load(cuda::std::memory_order_relaxed);
+    tail_cache = aref_u64(R.ctl[0]).load(cuda::std::memory_order_relaxed);
     if (idx + 1ull <= tail_cache + R.cap_mask + 1ull) break;
-    if (aref_sys_u64(R.ctl[1]).load(cuda::std::memory_order_relaxed) ||
+    if (aref_u64(R.ctl[1]).load(cuda::std::memory_order_relaxed) ||
         ld_relaxed(&a.L.lb->error)) {
       raise_error(a.L.lb, WM_ESHUTDOWN);
       return false;
@@ -657,13 +671,14 @@ __device__ __forceinline__ bool emit_one(const MotifArgs &a, unsigned long long 
     if (sl < 8192) sl <<= 1;
   }
   uint32_t *slot = R.slots + (idx & R.cap_mask) * R.stride;
+  slot[0] = (uint32_t)(idx + 1ull);
   slot[1] = (uint32_t)e;
   slot[2] = mask;
   slot[3] = (uint32_t)bm;
   slot[4] = (uint32_t)(bm >> 32);
   for (int j = 0; j < a.k - 1; ++j) slot[5 + j] = (uint32_t)tr[j];
-  __threadfence_system();
-  aref_sys_u32(slot[0]).store((uint32_t)(idx + 1ull), cuda::std::memory_order_relaxed);
+  __threadfence();
+  atomicAdd(R.blockdone + ((idx >> R.block_shift) & (R.cap_mask >> R.block_shift)), 1u);
   return true;
 }
 
@@ -873,26 +888,45 @@ static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s
   return WM_OK;
 }
 
-// Host side of the listing ring: mapped pinned memory cached in the
-// workspace, drained on the calling thread while the kernel runs.
+// Host side of the listing ring, cached per device: a mapped control block
+// (tail, failure flag), pinned staging for records and block counters, and a
+// copy stream so the copy engine drains the HBM ring while the kernel runs.
 struct HostRing {
-  uint32_t *slots = nullptr;
-  unsigned long long *ctl = nullptr;
-  size_t bytes = 0;
+  unsigned long long *ctl = nullptr;  // mapped [0] tail [1] failed
+  uint32_t *stage = nullptr;          // pinned [cap * stride]
+  uint32_t *counts = nullptr;         // pinned [cap >> block_shift]
+  size_t stage_bytes = 0, count_bytes = 0;
+  cudaStream_t copy = nullptr;
 };
 static HostRing g_hring[64];
 
-static int host_ring_get(Graph *g, unsigned long long cap, uint32_t stride, HostRing **out) {
+static int host_ring_get(Graph *g, unsigned long long cap, uint32_t stride, uint32_t nblk,
+                         HostRing **out) {
   HostRing &h = g_hring[g->device];
-  const size_t want = 256 + sizeof(uint32_t) * (size_t)cap * stride;
-  if (h.bytes < want) {
-    if (h.ctl) cudaFreeHost(h.ctl);
-    h = HostRing();
+  if (!h.ctl) {
     void *p = nullptr;
-    WM_CUDA(cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable));
+    WM_CUDA(cudaHostAlloc(&p, 256, cudaHostAllocMapped | cudaHostAllocPortable));
     h.ctl = static_cast<unsigned long long *>(p);
-    h.slots = reinterpret_cast<uint32_t *>(static_cast<char *>(p) + 256);
-    h.bytes = want;
+    WM_CUDA(cudaStreamCreateWithFlags(&h.copy, cudaStreamNonBlocking));
+  }
+  const size_t want = sizeof(uint32_t) * (size_t)cap * stride;
+  if (h.stage_bytes < want) {
+    if (h.stage) cudaFreeHost(h.stage);
+    h.stage = nullptr;
+    h.stage_bytes = 0;
+    void *p = nullptr;
+    WM_CUDA(cudaHostAlloc(&p, want, cudaHostAllocPortable));
+    h.stage = static_cast<uint32_t *>(p);
+    h.stage_bytes = want;
+  }
+  if (h.count_bytes < sizeof(uint32_t) * nblk) {
+    if (h.counts) cudaFreeHost(h.counts);
+    h.counts = nullptr;
+    h.count_bytes = 0;
+    void *p = nullptr;
+    WM_CUDA(cudaHostAlloc(&p, sizeof(uint32_t) * nblk, cudaHostAllocPortable));
+    h.counts = static_cast<uint32_t *>(p);
+    h.count_bytes = sizeof(uint32_t) * nblk;
   }
   *out = &h;
   return WM_OK;
@@ -918,64 +952,116 @@ static uint64_t record_hash(const uint32_t *r, int k) {
   return h;
 }
 
-// Drain records until the kernel (event `done`) has finished and every
-// ticket it handed out is consumed.
+// Consume records [0, n) of the staging buffer: checksum (all host cores)
+// and the sink; returns false when the sink failed.
+static bool consume(const uint32_t *recs, unsigned long long n, uint32_t stride, int k,
+                    wm_listing *lst, uint64_t &sum) {
+  uint64_t bsum = 0;
+  const long long nn = (long long)n;
+#pragma omp parallel for reduction(+ : bsum) schedule(static) if (nn >= 4096)
+  for (long long r = 0; r < nn; ++r) bsum += record_hash(recs + r * stride, k);
+  sum += bsum;
+  return !(lst->sink && lst->sink(lst->user, recs, n, stride) != 0);
+}
+
+// Drain the HBM ring while the kernel (event `done`) runs: poll the block
+// counters from the tail, copy every run of completed blocks with the copy
+// engine, reset their counters, publish the new tail.  After the kernel has
+// finished, the last partial block is copied up to the device head.
 static int drain_listing(HostRing *h, unsigned long long cap, uint32_t stride, int k,
-                         wm_listing *lst, cudaEvent_t done) {
+                         wm_listing *lst, cudaEvent_t done, const uint32_t *dring,
+                         uint32_t *dcounts, uint32_t block_shift,
+                         const unsigned long long *dhead, unsigned long long *dctl) {
+  const unsigned long long G = 1ull << block_shift, mask = cap - 1;
+  const uint32_t nblk = (uint32_t)(cap >> block_shift);
+  cudaStream_t cs = h->copy;
   unsigned long long tail = 0;
-  const unsigned long long mask = cap - 1;
   bool failed = false;
   uint64_t sum = 0, emitted = 0;
   int idle = 0;
-  const unsigned long long batch_max = cap / 4 > 0 ? cap / 4 : 1;
+  const char *dbg = getenv("WM_LIST_DEBUG");
+  double t_poll = 0, t_copy = 0, t_consume = 0;
+  long iters = 0, copies = 0;
+  auto now = []() {
+    struct timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec + 1e-9 * ts.tv_nsec;
+  };
+  double t0 = now();
   for (;;) {
-    unsigned long long avail = 0;
-    // after a sink failure the tail stops: producers block, see ctl[1], stop
-    while (!failed && avail < batch_max) {
-      const unsigned long long idx = tail + avail;
-      const uint32_t seq = __atomic_load_n(&h->slots[(idx & mask) * stride], __ATOMIC_ACQUIRE);
-      if (seq != (uint32_t)(idx + 1)) break;
-      ++avail;
-    }
-    if (avail) {
-      idle = 0;
-      // contiguous runs (the ring may wrap once inside the batch)
-      unsigned long long done_n = 0;
-      while (done_n < avail) {
-        const unsigned long long first = (tail + done_n) & mask;
-        unsigned long long run = avail - done_n;
-        if (first + run > cap) run = cap - first;
-        const uint32_t *recs = h->slots + first * stride;
-        if (!failed) {
-          for (unsigned long long r = 0; r < run; ++r) sum += record_hash(recs + r * stride, k);
-          emitted += run;
-          if (lst->sink && lst->sink(lst->user, recs, run, stride) != 0) {
-            failed = true;
-            __atomic_store_n(&h->ctl[1], 1ull, __ATOMIC_RELEASE);
-          }
+    ++iters;
+    if (!failed) {
+      double ta = now();
+      const uint32_t b0 = (uint32_t)((tail >> block_shift) & (nblk - 1));
+      const uint32_t nchk = nblk - b0 < 64u ? nblk - b0 : 64u;  // no wrap inside one copy
+      WM_CUDA(cudaMemcpyAsync(h->counts, dcounts + b0, sizeof(uint32_t) * nchk,
+                              cudaMemcpyDeviceToHost, cs));
+      WM_CUDA(cudaStreamSynchronize(cs));
+      // counters accumulate G per lap and are never reset during the run (a
+      // reset would be a kernel on the copy stream, queued behind the
+      // persistent enumeration kernel): block b0 + i of lap L is complete
+      // when its counter reaches (L + 1) * G
+      const uint32_t want = (uint32_t)(((tail >> block_shift) / nblk + 1) * G);
+      uint32_t full = 0;
+      while (full < nchk && h->counts[full] == want) ++full;
+      double tb = now();
+      t_poll += tb - ta;
+      if (full) {
+        const unsigned long long n = (unsigned long long)full * G;
+        WM_CUDA(cudaMemcpyAsync(h->stage, dring + (tail & mask) * stride,
+                                sizeof(uint32_t) * stride * n, cudaMemcpyDeviceToHost, cs));
+        WM_CUDA(cudaStreamSynchronize(cs));
+        double tc = now();
+        t_copy += tc - tb;
+        ++copies;
+        const bool ok_c = consume(h->stage, n, stride, k, lst, sum);
+        t_consume += now() - tc;
+        if (ok_c) {
+          emitted += n;
+          tail += n;
+          h->ctl[0] = tail;  // pinned source of the H2D publish
+          WM_CUDA(cudaMemcpyAsync(dctl, &h->ctl[0], sizeof(unsigned long long),
+                                  cudaMemcpyHostToDevice, cs));
+        } else {
+          failed = true;  // the tail stops: producers block, see ctl[1], stop
+          h->ctl[1] = 1ull;
+          WM_CUDA(cudaMemcpyAsync(dctl + 1, &h->ctl[1], sizeof(unsigned long long),
+                                  cudaMemcpyHostToDevice, cs));
+          WM_CUDA(cudaStreamSynchronize(cs));
         }
-        done_n += run;
+        idle = 0;
+        continue;
       }
-      tail += avail;
-      __atomic_store_n(&h->ctl[0], tail, __ATOMIC_RELEASE);
-      continue;
     }
     const cudaError_t q = cudaEventQuery(done);
     if (q == cudaSuccess) {
-      if (failed) break;  // records left in the ring are discarded
-      // the kernel is complete: everything it wrote is visible; one more pass
-      const unsigned long long idx = tail;
-      const uint32_t seq = __atomic_load_n(&h->slots[(idx & mask) * stride], __ATOMIC_ACQUIRE);
-      if (seq == (uint32_t)(idx + 1)) continue;
+      if (!failed) {
+        unsigned long long head = 0;
+        WM_CUDA(cudaMemcpyAsync(&head, dhead, sizeof head, cudaMemcpyDeviceToHost, cs));
+        WM_CUDA(cudaStreamSynchronize(cs));
+        if (head > tail) {
+          // the block at the tail is the last, partial one (head - tail < G)
+          const unsigned long long n = head - tail;
+          WM_CUDA(cudaMemcpyAsync(h->stage, dring + (tail & mask) * stride,
+                                  sizeof(uint32_t) * stride * n, cudaMemcpyDeviceToHost, cs));
+          WM_CUDA(cudaStreamSynchronize(cs));
+          if (consume(h->stage, n, stride, k, lst, sum)) emitted += n;
+          else failed = true;
+          tail = head;
+        }
+      }
       break;
     }
-    if (q != cudaErrorNotReady) return fail(WM_ECUDA, "listing kernel failed: %s",
-                                           cudaGetErrorString(q));
-    if (++idle > 64) {
-      struct timespec ts = {0, 20000};
+    if (q != cudaErrorNotReady)
+      return fail(WM_ECUDA, "listing kernel failed: %s", cudaGetErrorString(q));
+    if (++idle > 4) {
+      struct timespec ts = {0, 10000};
       nanosleep(&ts, nullptr);
     }
   }
+  if (dbg && *dbg == '1')
+    fprintf(stderr, "[wm listing] %.3f ms total, %ld iters, %ld copies, poll %.3f copy %.3f consume %.3f ms\n",
+            1e3 * (now() - t0), iters, copies, 1e3 * t_poll, 1e3 * t_copy, 1e3 * t_consume);
   lst->emitted = emitted;
   lst->checksum = sum;
   lst->stride_words = stride;
@@ -1066,22 +1152,27 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   memset(&a.ring, 0, sizeof a.ring);
   HostRing *hr = nullptr;
   unsigned long long cap = 0;
+  uint32_t block_shift = 0;
   if (lst) {
-    cap = 64;
+    cap = 4096;
     while (cap < lst->capacity && cap < (1ull << 26)) cap <<= 1;
+    block_shift = 10;  // 1024-record completion blocks
+    const uint32_t nblk = (uint32_t)(cap >> block_shift);
     const uint32_t stride = (uint32_t)k + 4u;
-    if ((st = host_ring_get(g, cap, stride, &hr))) return st;
+    if ((st = host_ring_get(g, cap, stride, nblk, &hr))) return st;
     memset(hr->ctl, 0, 256);
-    for (unsigned long long i = 0; i < cap; ++i) hr->slots[i * stride] = 0u;
-    if ((st = g->ws->listing.ensure(sizeof(unsigned long long)))) return st;
-    WM_CUDA(cudaMemsetAsync(g->ws->listing.ptr, 0, sizeof(unsigned long long), s));
-    uint32_t *dslots = nullptr;
-    unsigned long long *dctl = nullptr;
-    WM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dslots), hr->slots, 0));
-    WM_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void **>(&dctl), hr->ctl, 0));
-    a.ring.slots = dslots;
-    a.ring.ctl = dctl;
+    // device block: [head u64][tail u64][failed u64][counters u32 x nblk]
+    if ((st = g->ws->listing.ensure(3 * sizeof(unsigned long long) +
+                                    sizeof(uint32_t) * (nblk + 2)))) return st;
+    if ((st = g->ws->listing_ring.ensure(sizeof(uint32_t) * cap * stride))) return st;
+    WM_CUDA(cudaMemsetAsync(g->ws->listing.ptr, 0,
+                            3 * sizeof(unsigned long long) + sizeof(uint32_t) * (nblk + 2), s));
+    unsigned long long *dctl = g->ws->listing.as<unsigned long long>() + 1;
+    a.ring.slots = g->ws->listing_ring.as<uint32_t>();
     a.ring.head = g->ws->listing.as<unsigned long long>();
+    a.ring.blockdone = reinterpret_cast<uint32_t *>(g->ws->listing.as<char>() + 24);
+    a.ring.block_shift = block_shift;
+    a.ring.ctl = dctl;
     a.ring.cap_mask = cap - 1;
     a.ring.stride = stride;
     a.ring.filter = lst->filter;
@@ -1111,7 +1202,8 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   int drain_st = WM_OK;
   if (lst) {
     // consume while the kernel produces (the host copies below would block)
-    drain_st = drain_listing(hr, cap, a.ring.stride, k, lst, k1);
+    drain_st = drain_listing(hr, cap, a.ring.stride, k, lst, k1, a.ring.slots,
+                             a.ring.blockdone, block_shift, a.ring.head, a.ring.ctl);
     if (drain_st == WM_ECUDA) return drain_st;
   }
   unsigned long long hc[8];
