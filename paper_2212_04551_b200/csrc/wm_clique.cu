@@ -429,6 +429,12 @@ __device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const u
 #ifndef WM_BULK4_MINK
 #define WM_BULK4_MINK 5
 #endif
+#ifndef WM_BULK5_MINK
+#define WM_BULK5_MINK 6
+#endif
+#ifndef WM_BULK5_POLL_MIN
+#define WM_BULK5_POLL_MIN 4
+#endif
 #ifndef WM_COMPACT_POLL_MIN
 #define WM_COMPACT_POLL_MIN 16
 #endif
@@ -706,6 +712,143 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
   return part;
 }
 
+// Five-level bulk for a node at traversal length k-5 whose candidate set has
+// m <= 32 members (always true for one-word roots): with R[x] the node's
+// one-word rows (the root's own rows when w = 1, else the compacted rows),
+//   leaves = sum_{h in P} sum_{i in C_h} sum_{j in C_hi} sum_{l in C_hij} popc(C_hij & R[l])
+// The (h, i, j) triples of ALL children h share one 64-entry ring, so rounds
+// stay full across sibling subtrees and the per-(k-4)-node work of bulk4
+// (compaction, child pops, partial rounds) disappears: the bulk4 node of each
+// child h is just the word C_h = c & R[h].  Returns false (nothing done) when
+// the node is too wide to compact; the DFS then continues to bulk4.
+__device__ __forceinline__ unsigned long long bulk5_round(const uint32_t *R, uint32_t c,
+                                                          const uint32_t *queue, int head,
+                                                          int nq) {
+  const int lane = lane_id();
+  unsigned long long part = 0;
+  if (lane < nq) {
+    const uint32_t e = queue[(head + lane) & 63];
+    const int h = (int)(e >> 10), i = (int)((e >> 5) & 31u), j = (int)(e & 31u);
+    const uint32_t cij = c & R[h] & R[i] & R[j];
+    uint32_t m = cij;
+    while (m) {
+      const int l = __ffs(m) - 1;
+      m &= m - 1u;
+      part += __popc(cij & R[l]);
+    }
+  }
+  return part;
+}
+
+template <int w, int WMAX>
+__device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int lv, int s0,
+                                      unsigned long long task, TaskCounters &tc, uint32_t &pt,
+                                      uint32_t &ph, unsigned long long &out) {
+  const int lane = lane_id();
+  const uint32_t *R;
+  uint32_t c, pc;
+  int m = 0, pos = -1;
+  if (w == 1) {
+    R = sm.adj;  // stride 1: the root's rows are already one word
+    c = sm.C[lv];
+    pc = sm.P[lv];
+  } else {
+#pragma unroll
+    for (int x = 0; x < w; ++x) m += __popc(sm.C[lv * w + x]);
+    if (m > 32) return false;
+    {
+      int before = 0;
+#pragma unroll
+      for (int x = 0; x < w; ++x) {
+        const uint32_t cw = sm.C[lv * w + x];
+        if ((cw >> lane) & 1u)
+          sm.crow[before + __popc(cw & ((1u << lane) - 1u))] = (uint32_t)(x * 32 + lane);
+        before += __popc(cw);
+      }
+    }
+    __syncwarp();
+    pos = lane < m ? (int)sm.crow[lane] : -1;
+    __syncwarp();
+    for (int r = 0; r < m; ++r) {
+      const int pr = __shfl_sync(0xffffffffu, pos, r);
+      const uint32_t *row = sm.adj + pr * w;
+      const bool bit = lane < m && ((row[pos >> 5] >> (pos & 31)) & 1u);
+      const unsigned bal = __ballot_sync(0xffffffffu, bit);
+      if (lane == 0) sm.crow[r] = bal;
+    }
+    pc = __ballot_sync(0xffffffffu,
+                       lane < m && ((sm.P[lv * w + (pos >> 5)] >> (pos & 31)) & 1u));
+    R = sm.crow;
+    c = m == 32 ? 0xffffffffu : ((1u << m) - 1u);
+    __syncwarp();
+  }
+  const bool pollable = a.lb_on && __popc(pc) >= WM_BULK5_POLL_MIN;
+  unsigned long long part = 0;
+  int head = 0, nq = 0;
+  while (pc) {
+    const int h = __ffs(pc) - 1;
+    pc &= pc - 1u;
+    const uint32_t ch = c & R[h];
+    uint32_t im = ch;
+    while (im) {
+      const int i = __ffs(im) - 1;
+      im &= im - 1u;
+      const uint32_t word = ch & R[i];
+      if ((word >> lane) & 1u)
+        sm.queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] =
+            ((uint32_t)h << 10) | ((uint32_t)i << 5) | (uint32_t)lane;
+      nq += __popc(word);
+      if (nq >= 32) {
+        __syncwarp();
+        part += bulk5_round(R, c, sm.queue, head, 32);
+        __syncwarp();
+        head = (head + 32) & 63;
+        nq -= 32;
+      }
+    }
+    if (pollable && ++tc.poll >= a.lb_poll) {
+      tc.poll = 0;
+      ++tc.polls;
+      int want = 0;
+      if (lane == 0) {
+        want = (int)(pt - ph) >= a.idle_min;
+        pt = (uint32_t)ld_relaxed(&a.L.lb->tail);
+        ph = (uint32_t)ld_relaxed(&a.L.lb->head);
+      }
+      if (__shfl_sync(0xffffffffu, want, 0)) {
+        // expose the pending children in the original bit space, donate,
+        // take back what is left
+        if (w == 1) {
+          if (lane == 0) sm.P[lv] = pc;
+          __syncwarp();
+          try_donate<w>(sm.C, sm.P, a, s0, lv, task);
+          pc = sm.P[lv];
+        } else {
+          const bool mine = lane < m && ((pc >> lane) & 1u);
+#pragma unroll
+          for (int x = 0; x < w; ++x) {
+            const uint32_t v =
+                __reduce_or_sync(0xffffffffu, (mine && (pos >> 5) == x) ? 1u << (pos & 31) : 0u);
+            if (lane == 0) sm.P[lv * w + x] = v;
+          }
+          __syncwarp();
+          try_donate<w>(sm.C, sm.P, a, s0, lv, task);
+          pc = __ballot_sync(0xffffffffu,
+                             lane < m && ((sm.P[lv * w + (pos >> 5)] >> (pos & 31)) & 1u));
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (nq) {
+    __syncwarp();
+    part += bulk5_round(R, c, sm.queue, head, nq);
+    __syncwarp();
+  }
+  out = part;
+  return true;
+}
+
 // Process one task (root or donated level) of word width w.
 template <int w, int WMAX, bool BYTES>
 #ifdef WM_RUNTASK_INLINE
@@ -774,6 +917,15 @@ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
     pt = (uint32_t)ld_relaxed(&a.L.lb->tail);
     ph = (uint32_t)ld_relaxed(&a.L.lb->head);
   }
+  if (!BYTES && k >= WM_BULK5_MINK && s0 == k - 5) {
+    // the task itself is a five-level bulk node (if it compacts)
+    unsigned long long part = 0;
+    if (bulk5<w, WMAX>(sm, a, s0, s0, task, tc, pt, ph, part)) {
+      tc.acc += part;
+      tcio = tc;
+      return;
+    }
+  }
   if (!BYTES && k >= WM_BULK4_MINK && s0 == k - 4) {
     // the task itself is a four-level bulk node
     tc.acc += bulk4<w, WMAX>(sm, a, s0, s0, task, tc, pt, ph);
@@ -825,7 +977,17 @@ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
     const int cnt = __reduce_add_sync(0xffffffffu, __popc(cw));
     __syncwarp();
     ++tc.nodes;
-    if (cnt >= k - s - 1) {
+    unsigned long long part5 = 0;
+    bool done5 = false;
+    if (!BYTES && k >= WM_BULK5_MINK && s + 1 == k - 5 && cnt >= k - s - 1) {
+      if (lane < w) P[(s + 1) * w + lane] = cw;
+      __syncwarp();
+      done5 = bulk5<w, WMAX>(sm, a, s + 1, s0, task, tc, pt, ph, part5);
+      tc.acc += part5;
+    }
+    if (done5) {
+      // the child node was finished in bulk
+    } else if (cnt >= k - s - 1) {
       if (!BYTES && k >= WM_BULK4_MINK && s + 1 == k - 4) {
         if (lane < w) P[(s + 1) * w + lane] = cw;
         __syncwarp();
