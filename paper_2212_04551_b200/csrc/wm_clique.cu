@@ -435,6 +435,9 @@ __device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const u
 #ifndef WM_BULK5_POLL_MIN
 #define WM_BULK5_POLL_MIN 4
 #endif
+#ifndef WM_BULK5_POLL_EVERY
+#define WM_BULK5_POLL_EVERY 4
+#endif
 #ifndef WM_COMPACT_POLL_MIN
 #define WM_COMPACT_POLL_MIN 16
 #endif
@@ -806,7 +809,9 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
         nq -= 32;
       }
     }
-    if (pollable && ++tc.poll >= a.lb_poll) {
+    // a bulk5 child is a whole (k-4)-node: poll every WM_BULK5_POLL_EVERY
+    // children (the pipelined loads keep it cheap; every child over-donates)
+    if (pollable && ++tc.poll >= WM_BULK5_POLL_EVERY) {
       tc.poll = 0;
       ++tc.polls;
       int want = 0;
