@@ -342,6 +342,16 @@ __device__ __forceinline__ unsigned long long outdeg_bytes(const CliqueArgs &a, 
   return 4ull * (unsigned long long)(__ldg(a.doff + u + 1) - __ldg(a.doff + u));
 }
 
+// Pop the highest member of m (one FLO via bfind; __ffs needs BREV + FLO and
+// 31 - __clz is not folded back).  Sums of popcounts do not depend on the
+// member order.
+__device__ __forceinline__ int pop_hi(uint32_t &m) {
+  int l;
+  asm("bfind.u32 %0, %1;" : "=r"(l) : "r"(m));
+  m ^= 1u << l;
+  return l;
+}
+
 // Two-level bulk (traversal length k-2, k == 3 roots): sum_j popc(C & A[j]).
 template <int w, bool BYTES>
 __device__ __forceinline__ unsigned long long bulk2(const uint32_t *adj, const uint32_t *Cs,
@@ -401,13 +411,12 @@ __device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const u
         cnt += __popc(cj[x]);
       }
       if (cnt >= 2) {
-        unsigned long long sub = 0;
+        uint32_t sub = 0;  // <= (32 w)^2
 #pragma unroll
         for (int y = 0; y < w; ++y) {
           uint32_t m = cj[y];
           while (m) {
-            const int l = y * 32 + __ffs(m) - 1;
-            m &= m - 1u;
+            const int l = y * 32 + pop_hi(m);
             uint32_t rl[w];
             load_row<w>(adj + l * S, rl);
             uint32_t t = 0;
@@ -456,7 +465,7 @@ __device__ __forceinline__ unsigned long long bulk4_round(const uint32_t *adj, c
                                                           const uint32_t *queue, int head, int nq) {
   constexpr int S = Width<w>::S;
   const int lane = lane_id();
-  unsigned long long part = 0;
+  uint32_t part = 0;  // <= 32 * 32 * w per round: no 64-bit adds in the loop
   if (lane < nq) {
     const uint32_t e = queue[(head + lane) & 63];
     const int i = (int)(e >> 16), j = (int)(e & 0xffffu);
@@ -469,14 +478,11 @@ __device__ __forceinline__ unsigned long long bulk4_round(const uint32_t *adj, c
     for (int y = 0; y < w; ++y) {
       uint32_t m = cij[y];
       while (m) {
-        const int l = y * 32 + __ffs(m) - 1;
-        m &= m - 1u;
+        const int l = y * 32 + pop_hi(m);
         uint32_t rl[w];
         load_row<w>(adj + l * S, rl);
-        uint32_t t = 0;
 #pragma unroll
-        for (int x = 0; x < w; ++x) t += __popc(cij[x] & rl[x]);
-        part += t;
+        for (int x = 0; x < w; ++x) part += __popc(cij[x] & rl[x]);
       }
     }
   }
@@ -728,17 +734,13 @@ __device__ __forceinline__ unsigned long long bulk5_round(const uint32_t *R, uin
                                                           const uint32_t *queue, int head,
                                                           int nq) {
   const int lane = lane_id();
-  unsigned long long part = 0;
+  uint32_t part = 0;  // <= 32 * 32 per round
   if (lane < nq) {
     const uint32_t e = queue[(head + lane) & 63];
     const int h = (int)(e >> 10), i = (int)((e >> 5) & 31u), j = (int)(e & 31u);
     const uint32_t cij = c & R[h] & R[i] & R[j];
     uint32_t m = cij;
-    while (m) {
-      const int l = __ffs(m) - 1;
-      m &= m - 1u;
-      part += __popc(cij & R[l]);
-    }
+    while (m) part += __popc(cij & R[pop_hi(m)]);
   }
   return part;
 }
