@@ -269,6 +269,7 @@ void wm_graph_destroy(void *gp) {
     cudaStream_t s = g->ws->own_stream;
     if (g->offsets) cudaFreeAsync(g->offsets, s);
     if (g->neighbors) cudaFreeAsync(g->neighbors, s);
+    if (g->ehash) cudaFreeAsync(g->ehash, s);
   }
   delete g;
 }

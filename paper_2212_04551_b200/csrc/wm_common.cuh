@@ -87,6 +87,9 @@ __device__ __forceinline__ int lower_bound_i(const T *a, int n, T x) {
 // probe shrinks the range to ~sqrt of itself — a 64K-entry hub row takes
 // ~5 dependent loads instead of 16.  Binary search finishes (and bounds the
 // cost on skewed rows).
+#ifndef WM_BSEARCH_BRANCHLESS
+#define WM_BSEARCH_BRANCHLESS 0
+#endif
 __device__ __forceinline__ bool row_contains(const int32_t *__restrict__ nbr, int64_t b,
                                              int64_t e, int32_t x) {
   if (e - b > WM_INTERP_MIN) {
@@ -107,6 +110,19 @@ __device__ __forceinline__ bool row_contains(const int32_t *__restrict__ nbr, in
     b = lo + 1;
     e = hi;
   }
+#if WM_BSEARCH_BRANCHLESS
+  // branchless lower bound with 32-bit offsets from the row start: lanes
+  // probing rows of equal length run the same iteration count, no early exits
+  const int32_t *row = nbr + b;
+  uint32_t len = (uint32_t)(e - b), pos = 0;
+  if (len == 0) return false;
+  while (len > 1) {
+    const uint32_t half = len >> 1;
+    pos = (__ldg(row + pos + half) <= x) ? pos + half : pos;
+    len -= half;
+  }
+  return __ldg(row + pos) == x;
+#else
   while (b < e) {
     int64_t mid = (b + e) >> 1;
     int32_t y = __ldg(nbr + mid);
@@ -114,6 +130,47 @@ __device__ __forceinline__ bool row_contains(const int32_t *__restrict__ nbr, in
     if (y < x) b = mid + 1; else e = mid;
   }
   return false;
+#endif
+}
+
+// ---------------------------------------------------------------------------
+// Edge hash set: every undirected edge {u, v} of the CSR as the key
+// min << 32 | max in an open-addressed table of 32-byte buckets (4 keys, one
+// L2 sector), load factor <= 1/2, linear probing over buckets.  Keys fill a
+// bucket's slots in order and are never deleted, so a bucket whose last slot
+// is empty ends the probe.  An adjacency test is one sector load (rarely two)
+// with no dependence on either endpoint's CSR row — against log2(degree)
+// dependent loads for a binary search — and the tests of one candidate
+// against several traversal vertices are independent loads in flight together.
+constexpr unsigned long long kEhEmpty = ~0ull;
+
+struct EdgeHash {
+  const ulonglong2 *b;        // bucket i = b[2i], b[2i+1]; null = no table (binary search)
+  unsigned long long bmask;
+};
+
+__device__ __host__ __forceinline__ unsigned long long eh_key(int32_t u, int32_t v) {
+  const uint32_t lo = (uint32_t)(u < v ? u : v), hi = (uint32_t)(u < v ? v : u);
+  return ((unsigned long long)lo << 32) | hi;
+}
+
+__device__ __host__ __forceinline__ unsigned long long eh_bucket(unsigned long long key,
+                                                                 unsigned long long bmask) {
+  unsigned long long z = key + 0x9E3779B97F4A7C15ull;  // splitmix64 finaliser
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return (z ^ (z >> 31)) & bmask;
+}
+
+__device__ __forceinline__ bool edge_hash_contains(const EdgeHash &H, int32_t u, int32_t v) {
+  const unsigned long long key = eh_key(u, v);
+  unsigned long long b = eh_bucket(key, H.bmask);
+  for (;;) {
+    const ulonglong2 p = __ldg(H.b + 2 * b), q = __ldg(H.b + 2 * b + 1);
+    if (p.x == key || p.y == key || q.x == key || q.y == key) return true;
+    if (q.y == kEhEmpty) return false;
+    b = (b + 1) & H.bmask;
+  }
 }
 
 using aref_u64 = cuda::atomic_ref<unsigned long long, cuda::thread_scope_device>;
@@ -347,7 +404,13 @@ struct Graph {
   int64_t *offsets = nullptr;   // device [n+1]
   int32_t *neighbors = nullptr; // device [nnz]
   Workspace *ws = nullptr;
+  // edge hash set (motif adjacency probes), built on first use; owned by the graph
+  unsigned long long *ehash = nullptr;
+  unsigned long long ehash_bmask = 0;  // bucket count - 1 (4 keys per bucket)
 };
+
+// builds g->ehash on stream s if absent (wm_motif.cu)
+int graph_edge_hash(Graph *g, cudaStream_t s);
 
 // Allocates the balancer's ring for `warps` and initialises lb (one
 // LbState) on stream s.

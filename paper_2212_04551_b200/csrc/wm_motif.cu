@@ -101,6 +101,7 @@ struct MotifArgs {
   unsigned long long *counters;    // [0] leaves [1] B_alg [2] tasks [3] nodes [4] polls [5] peak
   int lb_on, lb_poll, idle_min;
   int smem_hist;
+  EdgeHash H;                      // adjacency probes (null table: CSR binary search)
   LbShared L;
   ListRing ring;
 };
@@ -122,6 +123,35 @@ __device__ __forceinline__ int group_off(int i) { return i * (i - 1) / 2 - 1; }
 __device__ __forceinline__ bool adj_probe(const int32_t *__restrict__ nbr, int32_t e, long long eb,
                                           long long ee, int32_t x, long long xb, long long xe) {
   return (ee - eb <= xe - xb) ? row_contains(nbr, eb, ee, x) : row_contains(nbr, xb, xe, e);
+}
+
+// Adjacency of candidate e with traversal vertex tr[j]: one edge-hash probe;
+// without a table, a binary search in the shorter CSR row (e's bounds loaded
+// on first use into eb/ee).
+__device__ __forceinline__ bool adj_tr(const MotifArgs &a, const MotifWarp &w, int j, int32_t e,
+                                       long long &eb, long long &ee) {
+  if (a.H.b) return edge_hash_contains(a.H, e, w.tr[j]);
+  if (eb < 0) {
+    eb = __ldg(a.off + e);
+    ee = __ldg(a.off + e + 1);
+  }
+  return adj_probe(a.nbr, e, eb, ee, w.tr[j], w.tb[j], w.te[j]);
+}
+
+// e adjacent to none of tr[0..L): the B-part test.  With the hash table the L
+// probes are independent loads (no early exit), all in flight at once.
+__device__ __forceinline__ bool adj_none(const MotifArgs &a, const MotifWarp &w, int L, int32_t e) {
+  long long eb = -1, ee = -1;
+  if (a.H.b) {
+    bool hit = false;
+#pragma unroll
+    for (int j = 0; j < kMaxK - 1; ++j)
+      if (j < L) hit |= edge_hash_contains(a.H, e, w.tr[j]);
+    return !hit;
+  }
+  bool keep = true;
+  for (int j = 0; j < L && keep; ++j) keep = !adj_tr(a, w, j, e, eb, ee);
+  return keep;
 }
 
 __device__ __forceinline__ uint32_t *level_ptr(const MotifArgs &a, uint32_t *base, int L) {
@@ -203,8 +233,8 @@ __device__ __forceinline__ uint32_t build_next(const MotifArgs &a, MotifWarp &w,
       const uint32_t ent = __ldcg(src + i);
       const int32_t e = (int32_t)(ent & a.vmask);
       if (e > x) {
-        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
-        const bool hit = adj_probe(a.nbr, e, eb, ee, x, xb, xe);
+        long long eb = -1, ee = -1;
+        const bool hit = adj_tr(a, w, L, e, eb, ee);
         val = ent | ((uint32_t)hit << (a.vbits + L));
         keep = true;
       }
@@ -219,10 +249,7 @@ __device__ __forceinline__ uint32_t build_next(const MotifArgs &a, MotifWarp &w,
     if (p < xe) {
       const int32_t e = __ldg(a.nbr + p);
       if (e > t0) {
-        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
-        keep = true;
-        for (int j = 0; j < L && keep; ++j)
-          keep = !adj_probe(a.nbr, e, eb, ee, w.tr[j], w.tb[j], w.te[j]);
+        keep = adj_none(a, w, L, e);
         val = (uint32_t)e | (1u << (a.vbits + L));
       }
     }
@@ -230,6 +257,22 @@ __device__ __forceinline__ uint32_t build_next(const MotifArgs &a, MotifWarp &w,
   }
   return cnt;
 }
+
+// WM_MOTIF_PROF=1 (tuning builds only): per-phase SM cycles summed over warps
+// into counters[20..27] — [20] idle (acquire_work) [21] donated-prefix
+// rebuild [22] level builds [23] leaf aggregation [24] leaf steps [25] max
+// single leaf step [26] records received; [28..31] leaf-step candidates:
+// A scanned, A kept (e > x), B scanned, B kept — printed by run_motif.
+#ifndef WM_MOTIF_PROF
+#define WM_MOTIF_PROF 0
+#endif
+#if WM_MOTIF_PROF
+#define WM_PT(v) const long long v = clock64()
+#define WM_PACC(slot, t0) (prof[slot] += (unsigned long long)(clock64() - (t0)))
+#else
+#define WM_PT(v)
+#define WM_PACC(slot, t0)
+#endif
 
 // dictionary lookup (aggregate.py:189); SENTINEL >= pattern_count either way
 __device__ __forceinline__ uint32_t dict_lookup(const MotifArgs &a, uint32_t bits) {
@@ -271,9 +314,8 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
       const uint32_t ent = __ldcg(src + i);
       const int32_t e = (int32_t)(ent & a.vmask);
       if (e > x) {
-        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
-        const uint32_t mask =
-            (ent >> a.vbits) | ((uint32_t)adj_probe(a.nbr, e, eb, ee, x, xb, xe) << L);
+        long long eb = -1, ee = -1;
+        const uint32_t mask = (ent >> a.vbits) | ((uint32_t)adj_tr(a, w, L, e, eb, ee) << L);
         pid = dict_lookup(a, bits | (mask << off));
         valid = true;
         bad |= pid >= a.pattern_count;
@@ -283,17 +325,20 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     hist_add(a, sh, valid && pid < a.pattern_count, pid);
   }
   unsigned long long nb = 0;
-  for (long long p0 = row_first_above(a.nbr, xb, xe, t0); p0 < xe; p0 += 32) {
+  const long long pb = row_first_above(a.nbr, xb, xe, t0);
+#if WM_MOTIF_PROF
+  if (lane == 0) {
+    atomicAdd(&a.counters[28], (unsigned long long)n_src);
+    atomicAdd(&a.counters[29], total);
+    atomicAdd(&a.counters[30], (unsigned long long)(xe - pb));
+  }
+#endif
+  for (long long p0 = pb; p0 < xe; p0 += 32) {
     const long long p = p0 + lane;
     bool keep = false;
     if (p < xe) {
       const int32_t e = __ldg(a.nbr + p);
-      if (e > t0) {
-        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
-        keep = true;
-        for (int j = 0; j < L && keep; ++j)
-          keep = !adj_probe(a.nbr, e, eb, ee, w.tr[j], w.tb[j], w.te[j]);
-      }
+      if (e > t0) keep = adj_none(a, w, L, e);
     }
     nb += __popc(__ballot_sync(0xffffffffu, keep));
   }
@@ -306,6 +351,9 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     }
   }
   if (__any_sync(0xffffffffu, bad) && lane == 0) raise_error(a.L.lb, WM_EINVARIANT);
+#if WM_MOTIF_PROF
+  if (lane == 0) atomicAdd(&a.counters[31], nb);
+#endif
   return total + nb;
 }
 
@@ -415,8 +463,8 @@ __device__ __forceinline__ unsigned long long list_leaves(const MotifArgs &a, Mo
       const uint32_t ent = __ldcg(src + i);
       e = (int32_t)(ent & a.vmask);
       if (e > x) {
-        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
-        mask = (ent >> a.vbits) | ((uint32_t)adj_probe(a.nbr, e, eb, ee, x, xb, xe) << L);
+        long long eb = -1, ee = -1;
+        mask = (ent >> a.vbits) | ((uint32_t)adj_tr(a, w, L, e, eb, ee) << L);
         valid = true;
       }
     }
@@ -432,12 +480,7 @@ __device__ __forceinline__ unsigned long long list_leaves(const MotifArgs &a, Mo
     int32_t e = 0;
     if (p < xe) {
       e = __ldg(a.nbr + p);
-      if (e > t0) {
-        const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
-        keep = true;
-        for (int j = 0; j < L && keep; ++j)
-          keep = !adj_probe(a.nbr, e, eb, ee, w.tr[j], w.tb[j], w.te[j]);
-      }
+      if (e > t0) keep = adj_none(a, w, L, e);
     }
     total += __popc(__ballot_sync(0xffffffffu, keep));
     const bool out = keep && (!complete_only || (prefix_full && (1u << L) == a.ring.full_mask));
@@ -458,8 +501,12 @@ __device__ __forceinline__ void set_tr(const MotifArgs &a, MotifWarp &w, int j, 
 
 constexpr int kMotifHdr = 6;  // [root, level, lo, hi, bitmap lo, bitmap hi] then tr[1..level)
 
+#ifndef WM_MOTIF_MINBLOCKS
+#define WM_MOTIF_MINBLOCKS 4
+#endif
+
 template <bool BYTES, bool LIST>
-__global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
+__global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(MotifArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned long long *sh = reinterpret_cast<unsigned long long *>(smraw);
   MotifWarp *warps = reinterpret_cast<MotifWarp *>(
@@ -481,12 +528,18 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
   bool ok = true;
   if (LIST && lane == 0) w.tail_cache = 0;
   int poll = 0;
+#if WM_MOTIF_PROF
+  unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#endif
   while (ok) {
     unsigned long long ti = 0;
     Rec3 rec = {{0u, 0u, 0u}};
+    WM_PT(tq);
     const int kind = acquire_work(a.L, a.lb_on, a.ntasks, roots_left, ti, rec, clk);
+    WM_PACC(0, tq);
     if (kind == 0) break;
     int s0;
+    WM_PT(tr0);
     if (kind == 1) {
       set_tr(a, w, 0, __ldg(a.tasks + a.task_offset + ti * a.task_stride));
       if (lane == 0) {
@@ -524,8 +577,12 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
         w.lo[s0] = lo;
         w.below[s0] = 0;
       }
+#if WM_MOTIF_PROF
+      prof[6] += 1;
+#endif
     }
     __syncwarp();
+    WM_PACC(kind == 1 ? 2 : 1, tr0);
     int s = s0;
     for (;;) {
       const uint32_t cur = w.cur[s];
@@ -558,12 +615,21 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
       ++nodes;
       if (s + 1 == k - 1) {
         unsigned long long got;
+        WM_PT(tl);
         if (LIST) {
           got = list_leaves(a, w, base, emitted, ok);
           if (!ok) break;
         } else {
           got = aggregate_leaves(a, w, base, sh);
         }
+#if WM_MOTIF_PROF
+        {
+          const unsigned long long d = (unsigned long long)(clock64() - tl);
+          prof[3] += d;
+          prof[4] += 1;
+          if (d > prof[5]) prof[5] = d;
+        }
+#endif
         leaves += got;
         if (BYTES && lane == 0 && got) {
           bytes += 4ull * (unsigned long long)(w.te[s] - w.tb[s]);
@@ -571,7 +637,9 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
         }
         __syncwarp();
       } else {
+        WM_PT(tb);
         const uint32_t n = build_next(a, w, base, s);
+        WM_PACC(2, tb);
         if ((long long)n > (long long)(s + 1) * a.maxdeg && lane == 0)
           raise_error(a.L.lb, WM_ECAPACITY);
         if (lane == 0) {
@@ -636,6 +704,12 @@ __global__ void __launch_bounds__(256) motif_enum_kernel(MotifArgs a) {
     atomicAdd(&a.counters[4], polls);
     atomicMax(&a.counters[5], peak);
     if (LIST) atomicAdd(&a.counters[6], emitted);
+#if WM_MOTIF_PROF
+    for (int q = 0; q < 7; ++q) {
+      if (q == 5) atomicMax(&a.counters[25], prof[5]);
+      else atomicAdd(&a.counters[20 + q], prof[q]);
+    }
+#endif
   }
   warp_clock_end(a.L.lb, clk);
   if (a.smem_hist) {
@@ -819,6 +893,56 @@ __global__ void __launch_bounds__(256) motif_dfs_kernel(MotifArgs a) {
     for (uint32_t i = threadIdx.x; i < a.pattern_count; i += blockDim.x)
       if (sh[i]) atomicAdd(a.hist + i, sh[i]);
   }
+}
+
+// Edge hash set construction (see EdgeHash): one warp per vertex u inserts the
+// keys of its neighbours v > u with atomicCAS, slots in order within a bucket.
+__global__ void edge_hash_build_kernel(int64_t n, const int64_t *__restrict__ off,
+                                       const int32_t *__restrict__ nbr,
+                                       unsigned long long *__restrict__ keys,
+                                       unsigned long long bmask) {
+  const int lane = lane_id();
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = wid; u < n; u += nw) {
+    const int64_t b = off[u], e = off[u + 1];
+    for (int64_t p = b + lane; p < e; p += 32) {
+      const int32_t v = nbr[p];
+      if (v <= (int32_t)u) continue;
+      const unsigned long long key = eh_key((int32_t)u, v);
+      unsigned long long bk = eh_bucket(key, bmask);
+      for (bool done = false; !done; bk = (bk + 1) & bmask) {
+        for (int sl = 0; sl < 4; ++sl) {
+          const unsigned long long prev = atomicCAS(keys + 4 * bk + sl, kEhEmpty, key);
+          if (prev == kEhEmpty || prev == key) { done = true; break; }
+        }
+      }
+    }
+  }
+}
+
+int graph_edge_hash(Graph *g, cudaStream_t s) {
+  if (g->ehash) return WM_OK;
+  const unsigned long long m = (unsigned long long)(g->nnz / 2);
+  unsigned long long slots = 64;
+  while (slots < 2 * m) slots <<= 1;  // load factor <= 1/2
+  const size_t bytes = slots * sizeof(unsigned long long);
+  void *p = nullptr;
+  cudaError_t e = cudaMallocFromPoolAsync(&p, bytes, g->ws->pool, s);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return WM_ECAPACITY;  // caller keeps the binary-search probes
+  }
+  WM_CUDA(cudaMemsetAsync(p, 0xFF, bytes, s));
+  const int64_t blocks = ((g->n * 32 + 255) / 256) < (int64_t)g->num_sms * 16
+                             ? (g->n * 32 + 255) / 256
+                             : (int64_t)g->num_sms * 16;
+  edge_hash_build_kernel<<<(int)(blocks > 0 ? blocks : 1), 256, 0, s>>>(
+      g->n, g->offsets, g->neighbors, static_cast<unsigned long long *>(p), slots / 4 - 1);
+  WM_CUDA(cudaGetLastError());
+  g->ehash = static_cast<unsigned long long *>(p);
+  g->ehash_bmask = slots / 4 - 1;
+  return WM_OK;
 }
 
 template <bool LIST>
@@ -1068,6 +1192,10 @@ static int drain_listing(HostRing *h, unsigned long long cap, uint32_t stride, i
   return failed ? WM_ESHUTDOWN : WM_OK;
 }
 
+#ifndef WM_EDGE_HASH
+#define WM_EDGE_HASH 1
+#endif
+
 int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s,
               wm_listing *lst) {
   const int64_t n = g->n;
@@ -1148,6 +1276,15 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   a.lb_poll = cfg->lb_poll > 0 ? cfg->lb_poll : 1;
   a.idle_min = 1;
   a.smem_hist = app->pattern_count <= 2048;
+  a.H.b = nullptr;
+  a.H.bmask = 0;
+  if (cfg->mode != WM_MODE_DFS && WM_EDGE_HASH) {
+    // built once per graph (first motif run), before the timed kernel
+    if (graph_edge_hash(g, s) == WM_OK) {
+      a.H.b = reinterpret_cast<const ulonglong2 *>(g->ehash);
+      a.H.bmask = g->ehash_bmask;
+    }
+  }
   a.L.lb = g->ws->lb.as<LbState>();
   memset(&a.ring, 0, sizeof a.ring);
   HostRing *hr = nullptr;
@@ -1208,6 +1345,10 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   }
   unsigned long long hc[8];
   WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
+#if WM_MOTIF_PROF
+  unsigned long long hp[12];
+  WM_CUDA(cudaMemcpyAsync(hp, ctr + 20, sizeof hp, cudaMemcpyDeviceToHost, s));
+#endif
   if (!lst)
     WM_CUDA(cudaMemcpyAsync(res->pattern_counts, g->ws->hist.ptr,
                             sizeof(unsigned long long) * app->pattern_count,
@@ -1223,6 +1364,14 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   res->d2h_bytes = sizeof ntask + sizeof hc + sizeof hl +
                    (lst ? (uint64_t)lst->emitted * a.ring.stride * 4
                         : sizeof(unsigned long long) * app->pattern_count);
+#if WM_MOTIF_PROF
+  fprintf(stderr,
+          "[motif prof] Gcycles idle %.3f rebuild %.3f build %.3f leaf %.3f | leaf steps %llu "
+          "max leaf step %.3f Mcycles | records %llu | A scanned %llu kept %llu B scanned %llu "
+          "kept %llu\n",
+          hp[0] * 1e-9, hp[1] * 1e-9, hp[2] * 1e-9, hp[3] * 1e-9, hp[4], hp[5] * 1e-6, hp[6],
+          hp[8], hp[9], hp[10], hp[11]);
+#endif
   res->leaves = hc[0];
   res->alg_bytes = bytes ? hc[1] : 0;
   res->tasks = hc[2];

@@ -31,3 +31,6 @@ for lib in sys.argv[4:]:
     out = subprocess.run([sys.executable, __file__, "--one", cfg, k, suffix], env=env,
                          capture_output=True, text=True)
     print(os.path.basename(lib), out.stdout.strip() or out.stderr[-500:], flush=True)
+    prof = [l for l in out.stderr.splitlines() if l.startswith("[motif prof]")]
+    if prof:
+        print("   ", prof[-1], flush=True)

@@ -1,2 +1,1 @@
-# A/B/C clique variants (build/variants/*.so), cfg3 at k=7,8,9
-for k in 8 7 9; do timeout 600 python scripts/ab_clique.py $k build/variants/A.so build/variants/B.so build/variants/C.so; done
+for lib in M0 MH; do for k in 4 5 6; do WM_B200_LIB=$PWD/build/variants/$lib.so timeout 300 python scripts/var_motif.py cfg2 $k 10; done; done
