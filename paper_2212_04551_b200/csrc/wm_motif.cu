@@ -946,7 +946,8 @@ int graph_edge_hash(Graph *g, cudaStream_t s) {
 }
 
 template <bool LIST>
-static int launch_motif_dfs(Graph *g, MotifArgs a, cudaStream_t s, int *warps_out, bool launch) {
+static int launch_motif_dfs(Graph *g, MotifArgs a, cudaStream_t s, int *warps_out, bool launch,
+                            cudaEvent_t k0) {
   const size_t smem = a.smem_hist ? ((size_t)a.pattern_count * 8 + 15) / 16 * 16 : 0;
   const unsigned long long per = a.warp_stride * sizeof(uint32_t);
   size_t free_b = 0, total_b = 0;
@@ -965,6 +966,7 @@ static int launch_motif_dfs(Graph *g, MotifArgs a, cudaStream_t s, int *warps_ou
   auto kern = motif_dfs_kernel<LIST>;
   if (smem > 48 * 1024)
     WM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  WM_CUDA(cudaEventRecord(k0, s));  // after all host-side setup: kernel time only
   kern<<<blocks, 256, smem, s>>>(a);
   WM_CUDA(cudaGetLastError());
   *warps_out = blocks * 8;
@@ -973,7 +975,7 @@ static int launch_motif_dfs(Graph *g, MotifArgs a, cudaStream_t s, int *warps_ou
 
 template <bool BYTES, bool LIST>
 static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s, int *warps_out,
-                        bool launch) {
+                        bool launch, cudaEvent_t k0) {
   int wpb = cfg->warps_per_block > 0 ? cfg->warps_per_block : 8;
   const size_t hist_bytes = a.smem_hist ? ((size_t)a.pattern_count * 8 + 15) / 16 * 16 : 0;
   const size_t smem = hist_bytes + sizeof(MotifWarp) * wpb;
@@ -1006,6 +1008,7 @@ static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s
   if ((st = lb_prepare(g, a.L.lb, warps, (uint32_t)(kMotifHdr + kMaxK), &a.L, s))) return st;
   a.idle_min = (int)((1.0 - cfg->lb_threshold) * warps);
   if (a.idle_min < 1) a.idle_min = 1;
+  WM_CUDA(cudaEventRecord(k0, s));  // after all host-side setup: kernel time only
   kern<<<(int)blocks, wpb * 32, smem, s>>>(a);
   WM_CUDA(cudaGetLastError());
   *warps_out = warps;
@@ -1321,11 +1324,11 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   int warps = 0;
   const bool dfs = cfg->mode == WM_MODE_DFS;
 #define WM_LAUNCH(GO)                                                            \
-  (dfs ? (lst ? launch_motif_dfs<true>(g, a, s, &warps, GO)                      \
-              : launch_motif_dfs<false>(g, a, s, &warps, GO)) :                  \
-  bytes ? launch_motif<true, false>(g, cfg, a, s, &warps, GO)                    \
-         : (lst ? launch_motif<false, true>(g, cfg, a, s, &warps, GO)            \
-                : launch_motif<false, false>(g, cfg, a, s, &warps, GO)))
+  (dfs ? (lst ? launch_motif_dfs<true>(g, a, s, &warps, GO, k0)                  \
+              : launch_motif_dfs<false>(g, a, s, &warps, GO, k0)) :              \
+  bytes ? launch_motif<true, false>(g, cfg, a, s, &warps, GO, k0)                \
+         : (lst ? launch_motif<false, true>(g, cfg, a, s, &warps, GO, k0)        \
+                : launch_motif<false, false>(g, cfg, a, s, &warps, GO, k0)))
   if (a.ntasks) {
     if ((st = WM_LAUNCH(false))) return st;
   }
