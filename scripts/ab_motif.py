@@ -14,7 +14,7 @@ if len(sys.argv) > 2 and sys.argv[1] == "--one":
     g = synth.config_graph(cfg)
     d = build_dictionary(k)
     roots = (g.n - suffix, g.n) if suffix else None
-    bc = BalanceConfig(threshold=0.9, poll_interval=int(os.environ.get("WM_POLL", "8")))
+    bc = BalanceConfig(threshold=float(os.environ.get("WM_THR", "0.9")), poll_interval=int(os.environ.get("WM_POLL", "8")))
     ms = []
     for i in range(4):
         r = run_motifs(g, k, d, mode="opt", balance_config=bc, roots=roots)

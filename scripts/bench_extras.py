@@ -55,8 +55,8 @@ for cfg, k, key in cases:
     want = golden[cfg]["motif_suffix"][key]
     roots = (g.n - want["suffix"], g.n)
     d = build_dictionary(k)
-    for mode, kw in (("wc", {}), ("opt", {"balance_config": BalanceConfig(threshold=0.9,
-                                                                          poll_interval=8)})):
+    for mode, kw in (("wc", {}), ("opt", {"balance_config": BalanceConfig(threshold=1.0,
+                                                                          poll_interval=2)})):
         r = best(lambda: run_motifs(g, k, d, mode=mode, roots=roots, **kw), 2)
         emit(what="%s motif root suffix" % cfg, k=k, suffix=want["suffix"], mode=mode,
              leaves=r.aggregated_total, matches_golden=r.pattern_counts == want["hist"],
@@ -75,7 +75,7 @@ for k in (4, 5, 6):
 # ---- listing: records streamed device -> mapped host ring -> consumer ------
 for cfg, k in (("cfg2", 6), ("cfg1", 6)):
     g = synth.config_graph(cfg)
-    lbc = BalanceConfig(threshold=0.9, poll_interval=8)
+    lbc = BalanceConfig(threshold=1.0, poll_interval=2)
     listing_checksum(g, k, mode="opt", balance_config=lbc)  # warm
     t = time.perf_counter()
     r = listing_checksum(g, k, mode="opt", balance_config=lbc)
