@@ -598,8 +598,7 @@ __device__ __forceinline__ unsigned long long bulk4_compact(CliqueSmem<WMAX> &sm
   unsigned long long part = 0;
   int head = 0, nq = 0;
   while (pc) {
-    const int i = __ffs(pc) - 1;
-    pc &= pc - 1u;
+    const int i = pop_hi(pc);
     const uint32_t word = sm.crow[i];  // row i is already restricted to C
     if ((word >> lane) & 1u)
       sm.queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] = ((uint32_t)i << 16) | (uint32_t)lane;
@@ -672,8 +671,7 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
   for (int q = 0; q < w; ++q) {
     uint32_t pm = Ps[q];  // pending children of word q, in a register between polls
     while (pm) {
-      const int i = q * 32 + __ffs(pm) - 1;
-      pm &= pm - 1u;
+      const int i = q * 32 + pop_hi(pm);
       uint32_t ci[w];
       load_row<w>(adj + i * S, ci);  // broadcast read
 #pragma unroll
@@ -791,13 +789,11 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
   unsigned long long part = 0;
   int head = 0, nq = 0;
   while (pc) {
-    const int h = __ffs(pc) - 1;
-    pc &= pc - 1u;
+    const int h = pop_hi(pc);
     const uint32_t ch = c & R[h];
     uint32_t im = ch;
     while (im) {
-      const int i = __ffs(im) - 1;
-      im &= im - 1u;
+      const int i = pop_hi(im);
       const uint32_t word = ch & R[i];
       if ((word >> lane) & 1u)
         sm.queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] =

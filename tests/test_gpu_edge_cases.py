@@ -45,14 +45,19 @@ def _check_motif(g, k, modes=("wc", "opt")):
         assert r.aggregated_total == want["leaves"], (k, mode)
 
 
-def _check_clique(g, k):
+def _check_clique(g, k, id_order=True):
     import oracle
-    from paper_2212_04551_b200 import BalanceConfig, run_clique
+    from paper_2212_04551_b200 import BalanceConfig, CapacityError, run_clique
     want = oracle.clique_fast(g, k)
     assert run_clique(g, k, mode="wc").clique_count == want, k
     bc = BalanceConfig(threshold=1.0, poll_interval=1)
     assert run_clique(g, k, mode="opt", balance_config=bc).clique_count == want, k
-    assert run_clique(g, k, mode="opt", balance_config=bc, order="id").clique_count == want, k
+    if id_order:
+        assert run_clique(g, k, mode="opt", balance_config=bc, order="id").clique_count == want, k
+    else:
+        # documented limit: a root's oriented row holds <= 1024 members
+        with pytest.raises(CapacityError):
+            run_clique(g, k, mode="opt", balance_config=bc, order="id")
 
 
 def test_graph_without_edges(cuda):
@@ -102,9 +107,10 @@ def test_hub_rows_motif(cuda, k, leaves, extra):
     _check_motif(_hub_graph(leaves, extra), k)
 
 
-@pytest.mark.parametrize("leaves,extra", [(600, 40000), (1500, 60000)])
+@pytest.mark.parametrize("leaves,extra", [(600, 40000), (1000, 50000), (1500, 60000)])
 def test_hub_rows_clique(cuda, leaves, extra):
-    # in id order the hub's out-row spans every leaf (wide bitmap classes)
+    # in id order the hub's out-row spans every leaf (wide bitmap classes, up to
+    # the 1024-member W=32 class); degree order puts the hubs last
     g = _hub_graph(leaves=leaves, extra=extra, seed=9)
     for k in (3, 4, 5, 6):
-        _check_clique(g, k)
+        _check_clique(g, k, id_order=leaves + 1 <= 1024)
