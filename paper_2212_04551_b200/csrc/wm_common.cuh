@@ -87,9 +87,6 @@ __device__ __forceinline__ int lower_bound_i(const T *a, int n, T x) {
 // probe shrinks the range to ~sqrt of itself — a 64K-entry hub row takes
 // ~5 dependent loads instead of 16.  Binary search finishes (and bounds the
 // cost on skewed rows).
-#ifndef WM_BSEARCH_BRANCHLESS
-#define WM_BSEARCH_BRANCHLESS 0
-#endif
 __device__ __forceinline__ bool row_contains(const int32_t *__restrict__ nbr, int64_t b,
                                              int64_t e, int32_t x) {
   if (e - b > WM_INTERP_MIN) {
@@ -110,19 +107,6 @@ __device__ __forceinline__ bool row_contains(const int32_t *__restrict__ nbr, in
     b = lo + 1;
     e = hi;
   }
-#if WM_BSEARCH_BRANCHLESS
-  // branchless lower bound with 32-bit offsets from the row start: lanes
-  // probing rows of equal length run the same iteration count, no early exits
-  const int32_t *row = nbr + b;
-  uint32_t len = (uint32_t)(e - b), pos = 0;
-  if (len == 0) return false;
-  while (len > 1) {
-    const uint32_t half = len >> 1;
-    pos = (__ldg(row + pos + half) <= x) ? pos + half : pos;
-    len -= half;
-  }
-  return __ldg(row + pos) == x;
-#else
   while (b < e) {
     int64_t mid = (b + e) >> 1;
     int32_t y = __ldg(nbr + mid);
@@ -130,7 +114,6 @@ __device__ __forceinline__ bool row_contains(const int32_t *__restrict__ nbr, in
     if (y < x) b = mid + 1; else e = mid;
   }
   return false;
-#endif
 }
 
 // ---------------------------------------------------------------------------

@@ -138,6 +138,10 @@ __device__ __forceinline__ bool adj_tr(const MotifArgs &a, const MotifWarp &w, i
   return adj_probe(a.nbr, e, eb, ee, w.tr[j], w.tb[j], w.te[j]);
 }
 
+#ifndef WM_BPART_UNROLL
+#define WM_BPART_UNROLL 6  // motif k <= 8 has L <= 6; deeper listing levels loop
+#endif
+
 // e adjacent to none of tr[0..L): the B-part test.  With the hash table the L
 // probes are independent loads (no early exit), all in flight at once.
 __device__ __forceinline__ bool adj_none(const MotifArgs &a, const MotifWarp &w, int L, int32_t e) {
@@ -145,8 +149,9 @@ __device__ __forceinline__ bool adj_none(const MotifArgs &a, const MotifWarp &w,
   if (a.H.b) {
     bool hit = false;
 #pragma unroll
-    for (int j = 0; j < kMaxK - 1; ++j)
+    for (int j = 0; j < WM_BPART_UNROLL; ++j)
       if (j < L) hit |= edge_hash_contains(a.H, e, w.tr[j]);
+    for (int j = WM_BPART_UNROLL; j < L; ++j) hit |= edge_hash_contains(a.H, e, w.tr[j]);
     return !hit;
   }
   bool keep = true;

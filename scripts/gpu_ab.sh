@@ -1,5 +1,2 @@
-L=paper_2212_04551_b200/libwm_b200.so
-for cfg in "cfg4 5 16384" "cfg5 7 32768" "cfg4 6 65536"; do
-for tp in "0.9 8" "1.0 8" "1.0 2" "0.95 4" "1.0 32"; do set -- $tp
-echo "thr $1 poll $2: $(WM_THR=$1 WM_POLL=$2 timeout 600 python scripts/ab_motif.py $cfg $L)"
-done; done
+WM_B200_LIB=$PWD/build/variants/CN.so timeout 900 python -m pytest tests/test_gpu_clique.py tests/test_gpu_edge_cases.py -m gpu -x -q 2>&1 | tail -n 2
+for k in 8 7 9 5; do timeout 600 python scripts/ab_clique.py $k build/variants/CP.so build/variants/CN.so; done
