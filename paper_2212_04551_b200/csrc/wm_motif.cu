@@ -125,17 +125,18 @@ __device__ __forceinline__ bool adj_probe(const int32_t *__restrict__ nbr, int32
   return (ee - eb <= xe - xb) ? row_contains(nbr, eb, ee, x) : row_contains(nbr, xb, xe, e);
 }
 
-// Adjacency of candidate e with traversal vertex tr[j]: one edge-hash probe;
-// without a table, a binary search in the shorter CSR row (e's bounds loaded
-// on first use into eb/ee).
-__device__ __forceinline__ bool adj_tr(const MotifArgs &a, const MotifWarp &w, int j, int32_t e,
-                                       long long &eb, long long &ee) {
-  if (a.H.b) return edge_hash_contains(a.H, e, w.tr[j]);
-  if (eb < 0) {
-    eb = __ldg(a.off + e);
-    ee = __ldg(a.off + e + 1);
-  }
+// Adjacency of candidate e with traversal vertex tr[j]: one edge-hash probe.
+// Without a table (allocation failed): binary search in the shorter CSR row,
+// out of line — a cold path whose interpolation search would otherwise be
+// inlined at every probe site of the hot loops.
+__device__ __noinline__ bool adj_csr(const MotifArgs &a, const MotifWarp &w, int j, int32_t e) {
+  const long long eb = __ldg(a.off + e), ee = __ldg(a.off + e + 1);
   return adj_probe(a.nbr, e, eb, ee, w.tr[j], w.tb[j], w.te[j]);
+}
+
+__device__ __forceinline__ bool adj_tr(const MotifArgs &a, const MotifWarp &w, int j, int32_t e) {
+  if (a.H.b) return edge_hash_contains(a.H, e, w.tr[j]);
+  return adj_csr(a, w, j, e);
 }
 
 #ifndef WM_BPART_UNROLL
@@ -145,7 +146,6 @@ __device__ __forceinline__ bool adj_tr(const MotifArgs &a, const MotifWarp &w, i
 // e adjacent to none of tr[0..L): the B-part test.  With the hash table the L
 // probes are independent loads (no early exit), all in flight at once.
 __device__ __forceinline__ bool adj_none(const MotifArgs &a, const MotifWarp &w, int L, int32_t e) {
-  long long eb = -1, ee = -1;
   if (a.H.b) {
     bool hit = false;
 #pragma unroll
@@ -155,7 +155,7 @@ __device__ __forceinline__ bool adj_none(const MotifArgs &a, const MotifWarp &w,
     return !hit;
   }
   bool keep = true;
-  for (int j = 0; j < L && keep; ++j) keep = !adj_tr(a, w, j, e, eb, ee);
+  for (int j = 0; j < L && keep; ++j) keep = !adj_csr(a, w, j, e);
   return keep;
 }
 
@@ -238,8 +238,7 @@ __device__ __forceinline__ uint32_t build_next(const MotifArgs &a, MotifWarp &w,
       const uint32_t ent = __ldcg(src + i);
       const int32_t e = (int32_t)(ent & a.vmask);
       if (e > x) {
-        long long eb = -1, ee = -1;
-        const bool hit = adj_tr(a, w, L, e, eb, ee);
+        const bool hit = adj_tr(a, w, L, e);
         val = ent | ((uint32_t)hit << (a.vbits + L));
         keep = true;
       }
@@ -319,8 +318,7 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
       const uint32_t ent = __ldcg(src + i);
       const int32_t e = (int32_t)(ent & a.vmask);
       if (e > x) {
-        long long eb = -1, ee = -1;
-        const uint32_t mask = (ent >> a.vbits) | ((uint32_t)adj_tr(a, w, L, e, eb, ee) << L);
+        const uint32_t mask = (ent >> a.vbits) | ((uint32_t)adj_tr(a, w, L, e) << L);
         pid = dict_lookup(a, bits | (mask << off));
         valid = true;
         bad |= pid >= a.pattern_count;
@@ -468,8 +466,7 @@ __device__ __forceinline__ unsigned long long list_leaves(const MotifArgs &a, Mo
       const uint32_t ent = __ldcg(src + i);
       e = (int32_t)(ent & a.vmask);
       if (e > x) {
-        long long eb = -1, ee = -1;
-        mask = (ent >> a.vbits) | ((uint32_t)adj_tr(a, w, L, e, eb, ee) << L);
+        mask = (ent >> a.vbits) | ((uint32_t)adj_tr(a, w, L, e) << L);
         valid = true;
       }
     }
@@ -1200,10 +1197,6 @@ static int drain_listing(HostRing *h, unsigned long long cap, uint32_t stride, i
   return failed ? WM_ESHUTDOWN : WM_OK;
 }
 
-#ifndef WM_EDGE_HASH
-#define WM_EDGE_HASH 1
-#endif
-
 int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s,
               wm_listing *lst) {
   const int64_t n = g->n;
@@ -1286,7 +1279,9 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   a.smem_hist = app->pattern_count <= 2048;
   a.H.b = nullptr;
   a.H.bmask = 0;
-  if (cfg->mode != WM_MODE_DFS && WM_EDGE_HASH) {
+  // WM_NO_EDGE_HASH=1 forces the CSR binary-search probes (fallback-path tests)
+  const char *no_hash = getenv("WM_NO_EDGE_HASH");
+  if (cfg->mode != WM_MODE_DFS && !(no_hash && *no_hash == '1')) {
     // built once per graph (first motif run), before the timed kernel
     if (graph_edge_hash(g, s) == WM_OK) {
       a.H.b = reinterpret_cast<const ulonglong2 *>(g->ehash);

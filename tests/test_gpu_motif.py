@@ -126,3 +126,15 @@ def test_cfg5_rmat_s22_root_suffix(scale_golden, cuda):
             kw = {"balance_config": BalanceConfig(threshold=1.0)} if mode == "opt" else {}
             r = run_motifs(g, k, dictionary(k), mode=mode, roots=(g.n - s, g.n), **kw)
             assert r.pattern_counts == want["hist"], (key, mode)
+
+
+def test_csr_probe_fallback_matches(golden, cuda, monkeypatch):
+    """Without the edge hash set (allocation failure path) the CSR binary-search
+    probes give the same histograms."""
+    from paper_2212_04551_b200 import run_motifs
+    monkeypatch.setenv("WM_NO_EDGE_HASH", "1")
+    for i, (g, e, r) in enumerate(_cases(golden)):
+        if i % 7:
+            continue
+        got = run_motifs(g, r["k"], dictionary(r["k"]), mode="opt")
+        assert got.pattern_counts == r["hist"], (e["name"], r["k"])
