@@ -32,6 +32,7 @@
 // shallowest pending extensions (balance.py:102-155 semantics: the thief owns
 // exactly the stolen branches; inherited levels are never regenerated).
 #include <cub/cub.cuh>
+#include <vector>
 
 #include "wm_common.cuh"
 
@@ -1300,7 +1301,160 @@ struct PhaseTimer {
   }
 };
 
+// --------------------------------------------------------------------------
+// Roots wider than the W=32 class (> 1024 out-neighbours): the k-cliques whose
+// lowest vertex is v are exactly {v} + the (k-1)-cliques of the subgraph
+// induced on N+(v), counted in any orientation.  Such roots are taken out of
+// the bitmap launch and each one's induced subgraph is counted by a nested
+// run (degree orientation inside it; nested wide roots recurse the same way).
+
+// warp per member i of the ascending member list M: how many of N(M[i]) are in M
+__global__ void induced_count_kernel(int d, const int32_t *__restrict__ M,
+                                     const int64_t *__restrict__ off,
+                                     const int32_t *__restrict__ nbr, int64_t *__restrict__ cnt) {
+  const int lane = lane_id();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < d; i += nw) {
+    const int32_t u = M[i];
+    int64_t c = 0;
+    for (int64_t p0 = off[u]; p0 < off[u + 1]; p0 += 32) {
+      const int64_t p = p0 + lane;
+      bool in = false;
+      if (p < off[u + 1]) {
+        const int32_t v = nbr[p];
+        const int j = lower_bound_i(M, d, v);
+        in = j < d && M[j] == v;
+      }
+      c += __popc(__ballot_sync(0xffffffffu, in));
+    }
+    if (lane == 0) cnt[i] = c;
+  }
+}
+
+// same walk, writing local ids in row order (ballot+popc keeps them ascending)
+__global__ void induced_fill_kernel(int d, const int32_t *__restrict__ M,
+                                    const int64_t *__restrict__ off,
+                                    const int32_t *__restrict__ nbr,
+                                    const int64_t *__restrict__ pos, int32_t *__restrict__ out) {
+  const int lane = lane_id();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < d; i += nw) {
+    const int32_t u = M[i];
+    int64_t w = pos[i];
+    for (int64_t p0 = off[u]; p0 < off[u + 1]; p0 += 32) {
+      const int64_t p = p0 + lane;
+      int j = d;
+      if (p < off[u + 1]) {
+        const int32_t v = nbr[p];
+        j = lower_bound_i(M, d, v);
+        if (j < d && M[j] != v) j = d;
+      }
+      const unsigned bal = __ballot_sync(0xffffffffu, j < d);
+      if (j < d) out[w + __popc(bal & ((1u << lane) - 1u))] = j;
+      w += __popc(bal);
+    }
+  }
+}
+
+static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res,
+                           cudaStream_t s, std::vector<std::vector<int32_t>> *wide);
+
+// count the (k-1)-cliques of G[M] for every wide root's member list and add
+// them (and the nested runs' statistics) into res
+static int clique_wide_roots(Graph *g, const wm_app *app, const wm_cfg *cfg,
+                             const std::vector<std::vector<int32_t>> &wide, wm_result *res,
+                             cudaStream_t s) {
+  for (const auto &M : wide) {
+    const int d = (int)M.size();
+    int32_t *dM = nullptr, *dnbr = nullptr;
+    int64_t *cnt = nullptr, *doff = nullptr;
+    void *tmp = nullptr;
+    size_t tb = 0;
+    WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, cnt, doff, d + 1, s));
+    WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&dM), sizeof(int32_t) * d,
+                                    g->ws->pool, s));
+    WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&cnt), sizeof(int64_t) * (d + 1),
+                                    g->ws->pool, s));
+    WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&doff), sizeof(int64_t) * (d + 1),
+                                    g->ws->pool, s));
+    WM_CUDA(cudaMallocFromPoolAsync(&tmp, tb, g->ws->pool, s));
+    WM_CUDA(cudaMemcpyAsync(dM, M.data(), sizeof(int32_t) * d, cudaMemcpyHostToDevice, s));
+    WM_CUDA(cudaMemsetAsync(cnt + d, 0, sizeof(int64_t), s));
+    const int blocks = (d * 32 + 255) / 256 < g->num_sms * 16 ? (d * 32 + 255) / 256
+                                                                : g->num_sms * 16;
+    induced_count_kernel<<<blocks, 256, 0, s>>>(d, dM, g->offsets, g->neighbors, cnt);
+    WM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, cnt, doff, d + 1, s));
+    std::vector<int64_t> hcnt(d + 1);
+    int64_t nnz = 0;
+    WM_CUDA(cudaMemcpyAsync(hcnt.data(), cnt, sizeof(int64_t) * d, cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaMemcpyAsync(&nnz, doff + d, sizeof nnz, cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaStreamSynchronize(s));
+    res->h2d_bytes += sizeof(int32_t) * d;
+    res->d2h_bytes += sizeof(int64_t) * (d + 1);
+    res->launches += 2;
+    int st = WM_OK;
+    if (app->k - 1 == 2) {
+      res->clique_count += (uint64_t)nnz / 2;  // 2-cliques of G[M]: its edges
+      res->leaves += (uint64_t)nnz / 2;
+    } else if (nnz > 0) {
+      WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&dnbr), sizeof(int32_t) * nnz,
+                                      g->ws->pool, s));
+      induced_fill_kernel<<<blocks, 256, 0, s>>>(d, dM, g->offsets, g->neighbors, doff, dnbr);
+      WM_CUDA(cudaGetLastError());
+      Graph sub;
+      sub.n = d;
+      sub.nnz = nnz;
+      for (int i = 0; i < d; ++i) sub.max_degree = hcnt[i] > sub.max_degree ? hcnt[i] : sub.max_degree;
+      sub.device = g->device;
+      sub.num_sms = g->num_sms;
+      sub.offsets = doff;
+      sub.neighbors = dnbr;
+      sub.ws = g->ws;
+      wm_app sa = *app;
+      sa.k = app->k - 1;
+      wm_cfg sc = *cfg;
+      sc.root_begin = sc.root_end = -1;
+      sc.shard_rank = 0;
+      sc.shard_count = 1;
+      sc.order = WM_ORDER_DEGREE;
+      wm_result r = {};
+      std::vector<std::vector<int32_t>> nested;
+      st = run_clique_impl(&sub, &sa, &sc, &r, s, &nested);
+      if (st == WM_OK && !nested.empty()) st = clique_wide_roots(&sub, &sa, &sc, nested, &r, s);
+      res->clique_count += r.clique_count;
+      res->leaves += r.leaves;
+      res->alg_bytes += r.alg_bytes;
+      res->nodes += r.nodes;
+      res->polls += r.polls;
+      res->kernel_ms += r.kernel_ms;
+      res->device_ms += r.device_ms;
+      res->build_ms += r.build_ms;
+      res->launches += r.launches + 1;
+      res->migrations += r.migrations;
+      res->rebalance_count += r.rebalance_count;
+      res->h2d_bytes += r.h2d_bytes;
+      res->d2h_bytes += r.d2h_bytes;
+    }
+    res->tasks += 1;
+    if (dnbr) cudaFreeAsync(dnbr, s);
+    cudaFreeAsync(tmp, s);
+    cudaFreeAsync(doff, s);
+    cudaFreeAsync(cnt, s);
+    cudaFreeAsync(dM, s);
+    if (st) return st;
+  }
+  return WM_OK;
+}
+
 int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s) {
+  std::vector<std::vector<int32_t>> wide;
+  int st = run_clique_impl(g, app, cfg, res, s, &wide);
+  if (st || wide.empty()) return st;
+  return clique_wide_roots(g, app, cfg, wide, res, s);
+}
+
+static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res,
+                           cudaStream_t s, std::vector<std::vector<int32_t>> *wide) {
   PhaseTimer pt(s);
   const int64_t n = g->n;
   const int k = app->k;
@@ -1407,11 +1561,31 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
     res->d2h_bytes = sizeof hb + sizeof key0 + sizeof hc;
     return WM_OK;
   }
-  if (hb[6]) {
-    return fail(WM_ECAPACITY,
-                "%llu root(s) have more than 1024 out-neighbours under this orientation "
-                "(use order=degree)", hb[6]);
+  // wide roots (> 1024 out-neighbours) sort first: hand this shard's share
+  // (cyclic over their own list) to clique_wide_roots, skip them below
+  const unsigned long long skip = hb[6];
+  if (skip) {
+    std::vector<int32_t> ids(skip);
+    WM_CUDA(cudaMemcpyAsync(ids.data(), g->ws->vals_out.ptr, sizeof(int32_t) * skip,
+                            cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaStreamSynchronize(s));
+    for (unsigned long long i = (unsigned long long)cfg->shard_rank; i < skip;
+         i += (unsigned long long)cfg->shard_count) {
+      int64_t be[2];
+      WM_CUDA(cudaMemcpyAsync(be, g->ws->dag_off.as<int64_t>() + ids[i], sizeof be,
+                              cudaMemcpyDeviceToHost, s));
+      WM_CUDA(cudaStreamSynchronize(s));
+      std::vector<int32_t> M((size_t)(be[1] - be[0]));
+      WM_CUDA(cudaMemcpyAsync(M.data(), g->ws->dag_nbr.as<int32_t>() + be[0],
+                              sizeof(int32_t) * M.size(), cudaMemcpyDeviceToHost, s));
+      WM_CUDA(cudaStreamSynchronize(s));
+      res->d2h_bytes += sizeof be + sizeof(int32_t) * M.size();
+      wide->push_back(std::move(M));
+    }
+    res->d2h_bytes += sizeof(int32_t) * skip;
   }
+  uint32_t *keys_sorted = g->ws->keys_out.as<uint32_t>() + skip;
+  int32_t *tasks_sorted = g->ws->vals_out.as<int32_t>() + skip;
   unsigned long long ntask = 0;
   for (int c = 0; c < 6; ++c) ntask += hb[c];
   // bitmap arena offsets: exclusive scan of d * ceil(d/32) over the sorted tasks
@@ -1419,7 +1593,7 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   unsigned long long *bm_off = g->ws->table.as<unsigned long long>();
   unsigned long long arena_words = 0;
   if (ntask) {
-    task_words_kernel<<<eblocks, tpb, 0, s>>>(ntask, g->ws->keys_out.as<uint32_t>(), words);
+    task_words_kernel<<<eblocks, tpb, 0, s>>>(ntask, keys_sorted, words);
     WM_CUDA(cudaMemsetAsync(words + ntask, 0, sizeof(unsigned long long), s));
     tb = g->ws->cub_tmp.bytes;
     WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, words, bm_off, (int)(ntask + 1), s));
@@ -1485,7 +1659,7 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
       CliqueArgs a;
       a.doff = g->ws->dag_off.as<int64_t>();
       a.dnbr = g->ws->dag_nbr.as<int32_t>();
-      a.tasks = g->ws->vals_out.as<int32_t>() + begin;
+      a.tasks = tasks_sorted + begin;
       a.bm_off = bm_off + begin;
       a.bm = g->ws->arena.as<uint32_t>();
       begin += cnt;
@@ -1513,7 +1687,7 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
       CliqueArgs a;
       a.doff = g->ws->dag_off.as<int64_t>();
       a.dnbr = g->ws->dag_nbr.as<int32_t>();
-      a.tasks = g->ws->vals_out.as<int32_t>() + cls[i].begin;
+      a.tasks = tasks_sorted + cls[i].begin;
       a.bm_off = bm_off + cls[i].begin;
       a.bm = g->ws->arena.as<uint32_t>();
       a.task_offset = (unsigned long long)cfg->shard_rank;
@@ -1559,8 +1733,8 @@ int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, c
   WM_CUDA(cudaEventElapsedTime(&kms, kb, k1));
   WM_CUDA(cudaEventElapsedTime(&dms, e0, e1));
   res->build_ms = bms;
-  res->d2h_bytes = sizeof hb + (ntask ? sizeof arena_words : 0) + sizeof hc +
-                   sizeof(LbState) * (uint64_t)launched;
+  res->d2h_bytes += sizeof hb + (ntask ? sizeof arena_words : 0) + sizeof hc +
+                    sizeof(LbState) * (uint64_t)launched;
   res->clique_count = hc[0];
   res->leaves = hc[0];
   res->alg_bytes = bytes ? hc[1] : 0;

@@ -45,19 +45,14 @@ def _check_motif(g, k, modes=("wc", "opt")):
         assert r.aggregated_total == want["leaves"], (k, mode)
 
 
-def _check_clique(g, k, id_order=True):
+def _check_clique(g, k):
     import oracle
-    from paper_2212_04551_b200 import BalanceConfig, CapacityError, run_clique
+    from paper_2212_04551_b200 import BalanceConfig, run_clique
     want = oracle.clique_fast(g, k)
     assert run_clique(g, k, mode="wc").clique_count == want, k
     bc = BalanceConfig(threshold=1.0, poll_interval=1)
     assert run_clique(g, k, mode="opt", balance_config=bc).clique_count == want, k
-    if id_order:
-        assert run_clique(g, k, mode="opt", balance_config=bc, order="id").clique_count == want, k
-    else:
-        # documented limit: a root's oriented row holds <= 1024 members
-        with pytest.raises(CapacityError):
-            run_clique(g, k, mode="opt", balance_config=bc, order="id")
+    assert run_clique(g, k, mode="opt", balance_config=bc, order="id").clique_count == want, k
 
 
 def test_graph_without_edges(cuda):
@@ -109,8 +104,21 @@ def test_hub_rows_motif(cuda, k, leaves, extra):
 
 @pytest.mark.parametrize("leaves,extra", [(600, 40000), (1000, 50000), (1500, 60000)])
 def test_hub_rows_clique(cuda, leaves, extra):
-    # in id order the hub's out-row spans every leaf (wide bitmap classes, up to
-    # the 1024-member W=32 class); degree order puts the hubs last
+    # in id order the hub's out-row spans every leaf: wide bitmap classes up to
+    # 1024 members, beyond that the wide-root path (induced subgraph of N+(v))
     g = _hub_graph(leaves=leaves, extra=extra, seed=9)
     for k in (3, 4, 5, 6):
-        _check_clique(g, k, id_order=leaves + 1 <= 1024)
+        _check_clique(g, k)
+
+
+@pytest.mark.parametrize("k", [3, 4])
+def test_wide_roots_in_degree_order(cuda, k):
+    """K_1040 under degree order (all degrees tie -> id order): roots 0..14 have
+    > 1024 out-neighbours; their induced subgraphs recurse (k=4 nests once more,
+    down to the k-1 = 2 edge count).  Sharded runs still partition them."""
+    from math import comb
+    from paper_2212_04551_b200 import complete_graph, run_clique
+    g = complete_graph(1040)
+    assert run_clique(g, k).clique_count == comb(1040, k)
+    parts = [run_clique(g, k, shard=(r, 3), reduce=False).clique_count for r in range(3)]
+    assert sum(parts) == comb(1040, k)
