@@ -297,7 +297,7 @@ template <int WMAX> struct alignas(16) CliqueSmem {  // 16B: uint4 row loads
   uint32_t P[kMaxK * WMAX];            // unconsumed members       [s * w + x]
   unsigned long long below[kMaxK];     // leaves under the level's node (B_alg)
   int32_t last[kMaxK];                 // vertex appended at the level
-  uint32_t queue[64];                  // bulk4 pair ring: (i << 16) | j
+  uint32_t queue[96];                  // bulk4/5 ring (64) + a scratch slot per lane
   uint32_t crow[32];                   // bulk4 node compacted to <= 32 members
 };
 
@@ -351,6 +351,14 @@ __device__ __forceinline__ int pop_hi(uint32_t &m) {
   asm("bfind.u32 %0, %1;" : "=r"(l) : "r"(m));
   m ^= 1u << l;
   return l;
+}
+
+// Branch-free ring push: the lanes whose bit is set in `word` take the next
+// ring positions in lane order; the others write their scratch slot 64 + lane.
+__device__ __forceinline__ int ring_slot(uint32_t word, int tail) {
+  const int lane = lane_id();
+  const uint32_t lt = (1u << lane) - 1u;
+  return ((word >> lane) & 1u) ? ((tail + __popc(word & lt)) & 63) : 64 + lane;
 }
 
 // Two-level bulk (traversal length k-2, k == 3 roots): sum_j popc(C & A[j]).
@@ -601,8 +609,7 @@ __device__ __forceinline__ unsigned long long bulk4_compact(CliqueSmem<WMAX> &sm
   while (pc) {
     const int i = pop_hi(pc);
     const uint32_t word = sm.crow[i];  // row i is already restricted to C
-    if ((word >> lane) & 1u)
-      sm.queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] = ((uint32_t)i << 16) | (uint32_t)lane;
+    sm.queue[ring_slot(word, head + nq)] = ((uint32_t)i << 16) | (uint32_t)lane;
     nq += __popc(word);
     if (nq >= 32) {
       __syncwarp();
@@ -679,9 +686,7 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
       for (int x = 0; x < w; ++x) {
         const uint32_t word = ci[x] & c[x];  // the child's candidates: its own ballot
         if (word == 0u) continue;
-        if ((word >> lane) & 1u)
-          queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] =
-              ((uint32_t)i << 16) | (uint32_t)(x * 32 + lane);
+        queue[ring_slot(word, head + nq)] = ((uint32_t)i << 16) | (uint32_t)(x * 32 + lane);
         nq += __popc(word);
         if (nq >= 32) {
           __syncwarp();
@@ -792,13 +797,12 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
   while (pc) {
     const int h = pop_hi(pc);
     const uint32_t ch = c & R[h];
+    const uint32_t hl = ((uint32_t)h << 10) | (uint32_t)lane;
     uint32_t im = ch;
     while (im) {
       const int i = pop_hi(im);
       const uint32_t word = ch & R[i];
-      if ((word >> lane) & 1u)
-        sm.queue[(head + nq + __popc(word & ((1u << lane) - 1u))) & 63] =
-            ((uint32_t)h << 10) | ((uint32_t)i << 5) | (uint32_t)lane;
+      sm.queue[ring_slot(word, head + nq)] = hl | ((uint32_t)i << 5);
       nq += __popc(word);
       if (nq >= 32) {
         __syncwarp();
