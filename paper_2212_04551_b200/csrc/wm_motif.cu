@@ -88,6 +88,12 @@ struct MotifArgs {
   const int32_t *nbr;
   const int32_t *tasks;
   unsigned long long ntasks, task_offset, task_stride;
+  // multi-GPU: every shard walks every root but descends only into the
+  // level-1 entries with index + root = l1_offset (mod l1_stride) (edge tasks
+  // (r, u) dealt cyclically, rotated by the root so the many one-child roots
+  // spread too); a hub root's subtree no longer lands on one
+  // GPU.  l1_stride = 1: no filter.
+  uint32_t l1_offset, l1_stride;
   int k;
   int vbits;
   uint32_t vmask;
@@ -600,6 +606,13 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
         __syncwarp();
         if (s == s0) break;
         --s;
+        continue;
+      }
+      if (s == 1 && a.l1_stride > 1 &&
+          ((cur - 1) + (uint32_t)w.tr[0]) % a.l1_stride != a.l1_offset) {
+        // another shard's edge task: consume without descending
+        if (lane == 0) w.cur[1] = cur - 1;
+        __syncwarp();
         continue;
       }
       // move_step: pop the highest pending entry (engine.py:652-669)
@@ -1257,8 +1270,17 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   a.off = g->offsets;
   a.nbr = g->neighbors;
   a.tasks = g->ws->vals_out.as<int32_t>();
-  a.task_offset = (unsigned long long)cfg->shard_rank;
-  a.task_stride = (unsigned long long)cfg->shard_count;
+  if (cfg->mode == WM_MODE_DFS) {  // the ablation kernel shards whole roots
+    a.task_offset = (unsigned long long)cfg->shard_rank;
+    a.task_stride = (unsigned long long)cfg->shard_count;
+    a.l1_offset = 0;
+    a.l1_stride = 1;
+  } else {
+    a.task_offset = 0;
+    a.task_stride = 1;
+    a.l1_offset = (uint32_t)cfg->shard_rank;
+    a.l1_stride = (uint32_t)cfg->shard_count;
+  }
   a.ntasks = ntask > a.task_offset ? (ntask - a.task_offset + a.task_stride - 1) / a.task_stride : 0;
   a.k = k;
   a.vbits = vbits;
