@@ -1531,7 +1531,8 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   tb = g->ws->cub_tmp.bytes;
   WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
       g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
-      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0, 32, s));
+      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0,
+      task_key_bits(g), s));
   bucket_count_kernel<<<eblocks, tpb, 0, s>>>(n, g->ws->keys_out.as<uint32_t>(), ctr + 8);
   pt.mark("task sort");
   unsigned long long hb[8];

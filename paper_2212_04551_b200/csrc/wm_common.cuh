@@ -392,6 +392,15 @@ struct Graph {
   unsigned long long ehash_bmask = 0;  // bucket count - 1 (4 keys per bucket)
 };
 
+// Task sort keys are (out-)degree + 1 <= max_degree + 1: radix-sort only those
+// bits (same stable order as a 32-bit sort, fewer passes).
+inline int task_key_bits(const Graph *g) {
+  unsigned long long v = (unsigned long long)g->max_degree + 1ull;
+  int b = 1;
+  while (b < 32 && (v >> b)) ++b;
+  return b;
+}
+
 // builds g->ehash on stream s if absent (wm_motif.cu)
 int graph_edge_hash(Graph *g, cudaStream_t s);
 

@@ -1261,7 +1261,8 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   size_t tb = g->ws->cub_tmp.bytes;
   WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
       g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
-      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0, 32, s));
+      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0,
+      task_key_bits(g), s));
   unsigned long long ntask = 0;
   WM_CUDA(cudaMemcpyAsync(&ntask, ctr + 8, sizeof ntask, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
