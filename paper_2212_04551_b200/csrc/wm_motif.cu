@@ -509,6 +509,10 @@ __device__ __forceinline__ void set_tr(const MotifArgs &a, MotifWarp &w, int j, 
 
 constexpr int kMotifHdr = 6;  // [root, level, lo, hi, bitmap lo, bitmap hi] then tr[1..level)
 
+// a leaf-level range is donated only if it carries >= this many candidate scans
+#ifndef WM_MOTIF_DONATE_MIN
+#define WM_MOTIF_DONATE_MIN 1024ull
+#endif
 #ifndef WM_MOTIF_MINBLOCKS
 #define WM_MOTIF_MINBLOCKS 4
 #endif
@@ -679,7 +683,8 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
             if (w.cur[j] - w.lo[j] >= 2u) { sd = j; break; }
           if (sd >= 0) {
             const uint32_t pend = w.cur[sd] - w.lo[sd];
-            const bool worth = sd < k - 2 || (unsigned long long)pend * w.size[sd] >= 4096ull;
+            const bool worth =
+                sd < k - 2 || (unsigned long long)pend * w.size[sd] >= WM_MOTIF_DONATE_MIN;
             if (worth) {
               const uint32_t half = pend / 2;
               const uint32_t lo = w.lo[sd];
