@@ -502,8 +502,11 @@ __device__ __forceinline__ unsigned long long bulk4_round(const uint32_t *adj, c
 // has any (reference balance.py:102-128 steals the shallowest pending entry;
 // one record here carries half of that level so a thief gets a large
 // subtree).  Record: [task, level, C[level] (w words), donated P (w words)].
-// Subtrees estimated below ~4K nodes are not worth a move and stay.
+// Subtrees estimated below ~16K nodes are not worth a move and stay.
 constexpr int kRecHdr = 2;
+#ifndef WM_CLIQUE_DONATE_MIN
+#define WM_CLIQUE_DONATE_MIN 16384.f
+#endif
 
 template <int w>
 __device__ __forceinline__ void try_donate(uint32_t *C, uint32_t *P, const CliqueArgs &a, int s0,
@@ -528,7 +531,7 @@ __device__ __forceinline__ void try_donate(uint32_t *C, uint32_t *P, const Cliqu
   const int csize = __reduce_add_sync(0xffffffffu, __popc(cw));
   const int depth = a.k - 2 - sd;  // levels below, bulk levels included
   const float est = (float)total * __powf((float)csize, (float)(depth - 1));
-  if (est < 4096.f) return;
+  if (est < WM_CLIQUE_DONATE_MIN) return;
   pre -= cnt;  // exclusive prefix
   const int keep = total / 2;
   uint32_t give;
