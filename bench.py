@@ -362,13 +362,17 @@ def secondary_workloads(stream):
     for k in (3, 4):
         r = run_clique(g1, k, stream=stream, shard=(0, 1))
         out["cfg1_clique_k%d" % k] = {"count": r.clique_count, "kernel_ms": r.kernel_ms}
+    from paper_2212_04551_b200 import BalanceConfig
     g2 = synth.config_graph("cfg2")
+    lb = BalanceConfig(threshold=1.0, poll_interval=2)
     for k in (4, 6):
-        run_motifs(g2, k, build_dictionary(k), stream=stream, shard=(0, 1))  # warm (lazy module load)
-        r = run_motifs(g2, k, build_dictionary(k), stream=stream, shard=(0, 1))
-        out["cfg2_motif_k%d" % k] = {"leaves": r.aggregated_total, "kernel_ms": r.kernel_ms,
-                                     "subgraphs_per_s": r.subgraphs_per_second,
-                                     "hist_head": r.pattern_counts[:6]}
+        for mode, kw in (("wc", {}), ("opt", {"balance_config": lb})):
+            run_motifs(g2, k, build_dictionary(k), mode=mode, stream=stream, shard=(0, 1), **kw)
+            r = run_motifs(g2, k, build_dictionary(k), mode=mode, stream=stream, shard=(0, 1), **kw)
+            out["cfg2_motif_k%d%s" % (k, "" if mode == "wc" else "_opt")] = {
+                "leaves": r.aggregated_total, "kernel_ms": r.kernel_ms,
+                "subgraphs_per_s": r.subgraphs_per_second, "hist_head": r.pattern_counts[:6],
+                "idle_warp_fraction": r.idle_warp_fraction}
     return out
 
 
