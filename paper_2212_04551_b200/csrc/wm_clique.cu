@@ -196,6 +196,8 @@ __global__ void task_words_kernel(unsigned long long ntask, const uint32_t *__re
 
 template <int W> struct BuildSmem {
   static constexpr int D = 32 * W;
+  unsigned long long key[D];  // orientation key of member i (rank-ordered bitmaps)
+  int32_t rk[D];              // member i's local index: its rank among the members
   int32_t list[D];
   uint32_t adj[D * W];
   int32_t pre[D + 1];
@@ -210,7 +212,9 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
                                                            const unsigned long long *__restrict__ bm_off,
                                                            uint32_t *__restrict__ bm,
                                                            unsigned long long first,
-                                                           unsigned long long stride) {
+                                                           unsigned long long stride,
+                                                           const int64_t *__restrict__ goff,
+                                                           int order, int rank_order) {
   extern __shared__ __align__(16) unsigned char smraw[];
   BuildSmem<W> &sm = reinterpret_cast<BuildSmem<W> *>(smraw)[threadIdx.x >> 5];
   const int lane = lane_id();
@@ -229,8 +233,27 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
       sm.list[i] = u;
       sm.rowbeg[i] = rb;
       sm.pre[i] = (int)(re - rb);
+      if (rank_order) {
+        const unsigned long long gd = order == WM_ORDER_ID ? 0ull
+                                          : (unsigned long long)(__ldg(goff + u + 1) - __ldg(goff + u));
+        sm.key[i] = (gd << 32) | (uint32_t)u;  // the orientation order of above()
+      }
     }
     for (int i = lane; i < d * wv; i += 32) sm.adj[i] = 0u;
+    __syncwarp();
+    // Local indices in descending orientation order make every row strictly
+    // lower-triangular (row i holds only members ranked above u_i, i.e. at
+    // smaller local indices), which the bulk loops exploit: the lowest member
+    // of a candidate set has no neighbour in it.
+    for (int i = lane; i < d; i += 32) {
+      int r = i;
+      if (rank_order) {
+        const unsigned long long ki = sm.key[i];
+        r = 0;
+        for (int j = 0; j < d; ++j) r += sm.key[j] > ki;
+      }
+      sm.rk[i] = r;
+    }
     __syncwarp();
     int carry = 0;
     for (int base = 0; base < d; base += 32) {
@@ -261,7 +284,7 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
             const int mid = (lo + hi) >> 1;
             if (sm.pre[mid] <= f) lo = mid; else hi = mid;
           }
-          rows[j] = lo;
+          rows[j] = sm.rk[lo];
           xs[j] = __ldg(dnbr + sm.rowbeg[lo] + (f - sm.pre[lo]));
         }
       }
@@ -269,8 +292,10 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
       for (int j = 0; j < 4; ++j) {
         if (rows[j] >= 0) {
           const int pos = lower_bound_i(sm.list, d, xs[j]);
-          if (pos < d && sm.list[pos] == xs[j])
-            atomicOr(&sm.adj[rows[j] * wv + (pos >> 5)], 1u << (pos & 31));
+          if (pos < d && sm.list[pos] == xs[j]) {
+            const int b = sm.rk[pos];
+            atomicOr(&sm.adj[rows[j] * wv + (b >> 5)], 1u << (b & 31));
+          }
         }
       }
     }
@@ -483,9 +508,14 @@ __device__ __forceinline__ unsigned long long bulk4_round(const uint32_t *adj, c
     load_row<w>(adj + j * S, rj);
 #pragma unroll
     for (int x = 0; x < w; ++x) cij[x] = c[x] & ri[x] & rj[x];
+    bool low = true;  // rows are lower-triangular: the lowest member adds nothing
 #pragma unroll
     for (int y = 0; y < w; ++y) {
       uint32_t m = cij[y];
+      if (low && m) {
+        m &= m - 1u;
+        low = false;
+      }
       while (m) {
         const int l = y * 32 + pop_hi(m);
         uint32_t rl[w];
@@ -747,6 +777,7 @@ __device__ __forceinline__ unsigned long long bulk5_round(const uint32_t *R, uin
     const int h = (int)(e >> 10), i = (int)((e >> 5) & 31u), j = (int)(e & 31u);
     const uint32_t cij = c & R[h] & R[i] & R[j];
     uint32_t m = cij;
+    m &= m - 1u;  // rows are lower-triangular: the lowest member adds nothing
     while (m) part += __popc(cij & R[pop_hi(m)]);
   }
   return part;
@@ -1216,7 +1247,8 @@ static int run_clique_dfs(Graph *g, const wm_cfg *cfg, int k, unsigned long long
 
 template <int W>
 static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask,
-                        unsigned long long first, unsigned long long stride, cudaStream_t s) {
+                        unsigned long long first, unsigned long long stride, int order,
+                        int rank_order, cudaStream_t s) {
   const size_t per_warp = sizeof(BuildSmem<W>);
   int wpb = 8;
   while (wpb > 1 && per_warp * wpb > 200 * 1024) wpb >>= 1;
@@ -1232,7 +1264,8 @@ static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask,
   const unsigned long long need = (mine + wpb - 1) / wpb;
   if (blocks > need) blocks = need;
   kern<<<(int)blocks, wpb * 32, smem, s>>>(a.doff, a.dnbr, a.tasks, ntask, a.bm_off,
-                                           const_cast<uint32_t *>(a.bm), first, stride);
+                                           const_cast<uint32_t *>(a.bm), first, stride,
+                                           g->offsets, order, rank_order);
   WM_CUDA(cudaGetLastError());
   return WM_OK;
 }
@@ -1682,7 +1715,7 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
       switch (c) {
 #define WM_BCASE(CC, WW) \
   case CC:               \
-    st = launch_build<WW>(g, a, cnt, first, N, s); \
+    st = launch_build<WW>(g, a, cnt, first, N, order, !bytes, s); \
     break;
         WM_BCASE(0, 1) WM_BCASE(1, 2) WM_BCASE(2, 4) WM_BCASE(3, 8) WM_BCASE(4, 16)
         WM_BCASE(5, 32)
