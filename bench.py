@@ -1,25 +1,37 @@
 #!/usr/bin/env python
 """Benchmark: subgraphs enumerated per second on B200 (BASELINE.json metric).
 
-Workload (a "step"): one full k-clique count of BASELINE config 3 — the
-Chung-Lu power-law graph with 100,000 vertices / 947,479 edges (SURVEY §8(d)
-recipe, seed 3) — through ``run_clique`` (clique_app pipeline) in ``opt`` mode
-(on-device load balancer on).  Default k=8 (9,384,222,498 cliques).  Counts
-are checked against the pinned golden value every step.
+Headline workload (a "step"): one full k-clique count of BASELINE config 3 —
+the Chung-Lu power-law graph with 100,000 vertices / 947,479 edges (SURVEY
+§8(d) recipe, seed 3) — through ``run_clique`` (clique_app pipeline) in
+``opt`` mode (on-device load balancer on).  Default k=8 (9,384,222,498
+cliques).  Counts are checked against the pinned golden value every step.
+
+At N=1 the same JSON line also carries the motif half of the metric
+(``motif`` block): configs 4 and 5 k-motif histograms over root suffixes,
+each timed the same way and checked against its golden histogram every step,
+with its algorithmic-byte roofline, LB-off/on idle fractions, e2e and CPU
+baseline.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--k 8]
-  python bench.py --impl reference ...   # CPU restatement of the reference
+  python bench.py --impl reference ...   # the reference algorithm on the host
 
-Multi-GPU: launched by torchrun, one process per GPU; rank r takes the
-cyclic share r (mod N) of the cost-sorted root tasks (no data-path
-collective); counts meet in ONE all_reduce; time = max over ranks.
+Multi-GPU: one process per GPU (torchrun, NCCL).  ``--gpus N`` without a
+torchrun environment re-launches itself under torchrun with N ranks (and
+fails if fewer than N GPUs are visible; ``WM_DIST_BACKEND=gloo`` lets ranks
+share GPUs for functional checks).  Rank r takes the cyclic share r (mod N)
+of the cost-sorted root tasks (no data-path collective); each step ends in
+ONE all_reduce of the device result vector; time = max over ranks.
 """
 
 from __future__ import annotations
 
 import argparse
+import glob
 import json
 import os
+import re
+import socket
 import statistics
 import subprocess
 import sys
@@ -31,6 +43,13 @@ sys.path.insert(0, ROOT)
 
 METRIC = "subgraphs enumerated/sec (k-clique, k-motif) at 1/2/4/8 B200 vs CPU ref"
 UNIT = "subgraphs/s"
+# fixed, seeded root subset the CPU reference runs to completion each step
+REF_ROOTS = 12000
+REF_SEED = 0
+# motif workloads of the N=1 line: (config, k, root suffix, LB-off suffix)
+MOTIF_WORKLOADS = (("cfg4", 5, 16384, 16384), ("cfg4", 6, 16384, 8192),
+                   ("cfg5", 7, 32768, None))
+MOTIF_CPU_ROOTS = {("cfg4", 5): 2048, ("cfg4", 6): 512, ("cfg5", 7): 512}
 
 
 def load_peaks():
@@ -42,24 +61,22 @@ def load_peaks():
         return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def golden_counts():
+def golden():
     try:
         with open(os.path.join(ROOT, "tests", "golden", "scale_golden.json")) as fh:
-            return json.load(fh).get("cfg3", {}).get("clique", {})
+            return json.load(fh)
     except Exception:
         return {}
 
 
-def ncu_traffic(k):
-    """dram bytes per launch of the enumeration kernel from the committed
-    ncu --set full capture (profiles/), or None."""
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+def ncu_figures():
+    """Per-launch figures of the dominant kernels from the committed ncu
+    --set full captures (profiles/ncu_traffic.json)."""
     try:
-        with open(path) as fh:
-            d = json.load(fh)
-        return d.get("clique_enum_kernel", {}).get("k%d" % k)
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            return json.load(fh)
     except Exception:
-        return None
+        return {}
 
 
 class ClockSampler:
@@ -78,7 +95,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -119,18 +136,6 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def dist_setup():
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    if world > 1:
-        import torch
-        import torch.distributed as dist
-        local = int(os.environ.get("LOCAL_RANK", "0"))
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl")
-    return rank, world
-
-
 def cpu_model():
     try:
         with open("/proc/cpuinfo") as fh:
@@ -142,45 +147,146 @@ def cpu_model():
     return "unknown"
 
 
-def cpu_sample(g, k, budget_s, seed=0):
-    """Reference algorithm (oracle/ C restatement of engine.run's clique
-    pipeline, id order) on all host cores over a seeded random root order,
-    time-boxed.  Returns (rate, leaves, seconds, roots_done, threads)."""
+# ---------------------------------------------------------------------------
+# multi-process launch
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def self_launch(args):
+    """``--gpus N`` outside torchrun: re-run this script under torchrun with
+    N ranks (one per GPU)."""
+    import torch
+    ndev = torch.cuda.device_count()
+    backend = os.environ.get("WM_DIST_BACKEND", "nccl")
+    if args.impl != "reference" and backend == "nccl" and ndev < args.gpus:
+        print("bench.py: --gpus %d but only %d GPU(s) visible (WM_DIST_BACKEND=gloo lets "
+              "ranks share GPUs for functional checks)" % (args.gpus, ndev), file=sys.stderr)
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           "--nproc-per-node=%d" % args.gpus, "--master-addr=127.0.0.1",
+           "--master-port=%d" % _free_port(), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def dist_setup(args):
+    """(rank, world, local_rank, backend) of this process; initialises the
+    process group for world > 1."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        print("bench.py: WORLD_SIZE=%d but --gpus %d" % (world, args.gpus), file=sys.stderr)
+        sys.exit(2)
+    import torch
+    ndev = torch.cuda.device_count()
+    backend = os.environ.get("WM_DIST_BACKEND", "nccl")
+    if ndev < 1:
+        print("bench.py: no CUDA device", file=sys.stderr)
+        sys.exit(2)
+    if world > 1:
+        if backend == "nccl" and ndev < world:
+            print("bench.py: %d ranks but %d GPU(s)" % (world, ndev), file=sys.stderr)
+            sys.exit(2)
+        torch.cuda.set_device(local % ndev)
+        # communicator log (nranks, NVLS) to a file: stdout carries one JSON line
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", "/tmp/wm_bench_nccl.%h.%p.log")
+        import torch.distributed as dist
+        dist.init_process_group(backend, device_id=torch.device("cuda", local % ndev)
+                                if backend == "nccl" else None)
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local, backend
+
+
+def nccl_evidence():
+    """nranks / NVLS lines from this process's NCCL log."""
+    paths = glob.glob("/tmp/wm_bench_nccl.*.%d.log" % os.getpid())
+    out = {"log": None, "nranks": None, "nvls": None}
+    for p in paths:
+        try:
+            txt = open(p, errors="replace").read()
+        except OSError:
+            continue
+        out["log"] = p
+        m = re.search(r"nranks (\d+)", txt)
+        if m:
+            out["nranks"] = int(m.group(1))
+        out["nvls"] = bool(re.search(r"NVLS", txt))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle restatement of the reference engine; test infra)
+
+
+def cpu_clique_subset(g, k, nroots=REF_ROOTS, seed=REF_SEED):
+    """The reference clique_app pipeline (oracle/wm_oracle.c restatement of
+    engine.py, id order) on all host cores over a FIXED seeded subset of
+    roots, run to completion.  Returns (rate, leaves, seconds, threads)."""
     import numpy as np
     import oracle
     threads = os.cpu_count() or 1
-    roots = np.random.default_rng(seed).permutation(g.n).astype(np.int64)
+    roots = np.random.default_rng(seed).permutation(g.n)[:nroots].astype(np.int64)
     t0 = time.perf_counter()
-    r = oracle.clique_run(g, k, roots=roots, threads=threads, time_budget_s=budget_s)
+    r = oracle.clique_run(g, k, roots=roots, threads=threads)
     dt = time.perf_counter() - t0
-    return r["leaves"] / dt, r["leaves"], dt, r["roots_done"], threads
+    return r["leaves"] / dt, r["leaves"], dt, threads
+
+
+def cpu_motif_subset(g, k, suffix, nroots, seed=REF_SEED):
+    """Reference motif_app pipeline (oracle restatement) over a fixed seeded
+    subset of the suffix's roots, all host cores, run to completion."""
+    import numpy as np
+    import oracle
+    from paper_2212_04551_b200 import build_dictionary
+    d = build_dictionary(k)
+    threads = os.cpu_count() or 1
+    lo = g.n - suffix
+    roots = (lo + np.random.default_rng(seed).permutation(suffix)[:nroots]).astype(np.int64)
+    t0 = time.perf_counter()
+    r = oracle.motif_run(g, k, d.table, d.pattern_count, roots=roots, threads=threads)
+    dt = time.perf_counter() - t0
+    return r["leaves"] / dt, r["leaves"], dt, threads
 
 
 def run_reference(args):
-    rank, world = dist_setup()
-    if rank != 0:
+    """``--impl reference``: the reference algorithm on the host cores (rank 0
+    only).  The graph is built on the host (WM_HOST_BUILD=1) so nothing of
+    the product library is loaded on this arm."""
+    os.environ["WM_HOST_BUILD"] = "1"
+    if int(os.environ.get("RANK", "0")) != 0:
         return 0
     from paper_2212_04551_b200 import synth
     g = synth.config_graph("cfg3")
-    per = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
     for _ in range(args.warmup):
-        cpu_sample(g, args.k, per, seed=1000 + _)
-    rates, leaves, secs, roots = [], 0, 0.0, 0
-    for i in range(args.steps):
-        rate, lv, dt, rd, threads = cpu_sample(g, args.k, per, seed=i)
+        cpu_clique_subset(g, args.k, args.ref_roots)
+    rates, leaves, secs = [], 0, 0.0
+    for _ in range(args.steps):
+        rate, lv, dt, threads = cpu_clique_subset(g, args.k, args.ref_roots)
         rates.append(rate)
         leaves += lv
         secs += dt
-        roots += rd
     value = leaves / secs if secs > 0 else 0.0
+    cv = statistics.pstdev(rates) / statistics.mean(rates) if rates and value > 0 else None
     sample = ("each step: reference clique_app pipeline (oracle/wm_oracle.c restatement of "
-              "engine.py:214-241, id order) over a seeded random permutation of the %d roots, "
-              "time-boxed to %.0f s; %d roots completed over %d steps" % (g.n, per, roots, args.steps))
+              "engine.py:214-241, id order) over the same fixed seeded subset of %d of the "
+              "%d roots (numpy default_rng(%d) permutation prefix), run to completion: %d "
+              "cliques per step" % (args.ref_roots, g.n, REF_SEED, leaves // max(1, args.steps)))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * secs / max(1, args.steps),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32/u64",
         "data": "synthetic", "config": workload_config(g, args.k, world),
+        "step_rate_cv": cv,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
                          "sample": sample, "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -194,8 +300,83 @@ def workload_config(g, k, world):
                         "seed 3)" % (k, g.n, g.m),
             "k": k, "app": "clique_app", "graph": "chung_lu(100000, 1000000, 2.3, seed=3)",
             "n": g.n, "m": g.m, "order": "degree", "mode": "opt",
-            "parallelism": "roots sharded cyclically over %d GPU(s)" % world,
+            "parallelism": "root tasks sharded cyclically over %d GPU(s), one all_reduce per step"
+                           % world,
             "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ---------------------------------------------------------------------------
+# timing helpers
+
+
+def timed_steps(step, steps, stream, flush, world):
+    """W warm-up steps are the caller's; here: K steps, each bracketed by CUDA
+    events on ``stream`` with an L2 flush (256 MiB write) before each; barrier
+    + synchronize on both sides.  Returns (per-step ms list, results, clocks)."""
+    import torch
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(steps)]
+    results = []
+    clocks = ClockSampler(torch.cuda.current_device())
+    if world > 1:
+        torch.distributed.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    for i in range(steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(i)  # outside the event pair
+        ev[i][0].record(stream)
+        results.append(step())
+        ev[i][1].record(stream)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    if world > 1:
+        torch.distributed.barrier()
+    return [a.elapsed_time(b) for a, b in ev], results, clk
+
+
+def max_over_ranks(vals, world):
+    if world == 1:
+        return vals
+    import torch
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+    return t.tolist()
+
+
+def e2e_steps(make_graph, step, steps, flush, world):
+    """End to end through the public API: a CsrGraph over pinned HOST arrays,
+    uploaded by ``wm_graph_create`` inside the step (plus validation, result
+    read-back); wall clock per step after a synchronize."""
+    import torch
+    from paper_2212_04551_b200 import engine
+    ms, results = [], []
+    if world > 1:
+        torch.distributed.barrier()
+    for i in range(steps):
+        flush.fill_(i)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        gh = make_graph()
+        r = step(gh)
+        engine.release_device_graph(gh)
+        torch.cuda.synchronize()
+        ms.append((time.perf_counter() - t0) * 1e3)
+        results.append(r)
+    return ms, results
+
+
+def _pinned_graph_factory(g):
+    import numpy as np
+    import torch
+    from paper_2212_04551_b200.graph import CsrGraph
+    off_h = torch.from_numpy(np.asarray(g.offsets)).pin_memory()
+    nbr_h = torch.from_numpy(np.asarray(g.neighbors_array)).pin_memory()
+    nbytes = off_h.numel() * 8 + nbr_h.numel() * 4
+    return (lambda: CsrGraph(g.n, off_h.numpy(), nbr_h.numpy())), nbytes
+
+
+# ---------------------------------------------------------------------------
 
 
 def main():
@@ -205,170 +386,259 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--k", type=int, default=8)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--no-extras", action="store_true")
+    ap.add_argument("--ref-roots", type=int, default=REF_ROOTS,
+                    help="fixed root subset of the CPU reference step")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--no-extras", action="store_true", help="skip LB/secondary evidence")
+    ap.add_argument("--no-motif", action="store_true", help="skip the motif block")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     if args.impl == "reference":
         return run_reference(args)
 
-    rank, world = dist_setup()
-    import numpy as np
+    rank, world, local, backend = dist_setup(args)
     import torch
-    from paper_2212_04551_b200 import BalanceConfig, engine, run_clique, synth
-    from paper_2212_04551_b200.graph import CsrGraph
-    dev = torch.cuda.current_device()
+    from paper_2212_04551_b200 import BalanceConfig, run_clique, synth
+    gold = golden()
     g = synth.config_graph("cfg3")
-    want = golden_counts().get(str(args.k), {}).get("count")
+    want = gold.get("cfg3", {}).get("clique", {}).get(str(args.k), {}).get("count")
     shard = (rank, world)
     bc = BalanceConfig(threshold=1.0, poll_interval=32)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()
 
-    def step(graph):
+    def step_on(graph):
         return run_clique(graph, args.k, mode="opt", balance_config=bc, shard=shard,
-                          stream=stream, reduce=False)
+                          stream=stream, reduce=True)
 
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device="cuda")
+    coll = None
+    if world > 1:
+        t = torch.ones(1, device="cuda")
+        torch.distributed.all_reduce(t)  # communicator up before timing
+        torch.cuda.synchronize()
+        coll = {"backend": backend, "world": world}
+        if backend == "nccl":
+            coll.update(nccl_evidence())
     for _ in range(args.warmup):
-        r = step(g)
+        step_on(g)
     # ---- timed: device-resident graph -------------------------------------
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
-    kern_ms, launches, results = [], 0, []
-    clocks = ClockSampler(dev)
-    if world > 1:
-        torch.distributed.barrier()
-    torch.cuda.synchronize()
-    clocks.start()
-    for i in range(args.steps):
-        flush.fill_(i)  # L2 flush, outside the event pair
-        ev[i][0].record(stream)
-        r = step(g)
-        ev[i][1].record(stream)
-        kern_ms.append(r.kernel_ms)
-        launches += r.launches
-        results.append(r)
-    torch.cuda.synchronize()
-    clk = clocks.stop()
-    step_ms = [a.elapsed_time(b) for a, b in ev]
-    total_ms = sum(step_ms)
-    if world > 1:
-        torch.distributed.barrier()
-        t = torch.tensor([total_ms, statistics.mean(kern_ms)], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms, kmean = t.tolist()
-        cnt = torch.tensor([sum(x.clique_count for x in results)], dtype=torch.int64, device="cuda")
-        torch.distributed.all_reduce(cnt)
-        all_leaves = int(cnt.item())
-    else:
-        kmean = statistics.mean(kern_ms)
-        all_leaves = sum(x.clique_count for x in results)
-    per_step_count = all_leaves // args.steps
+    step_ms, results, clk = timed_steps(lambda: step_on(g), args.steps, stream, flush, world)
+    total_ms = max_over_ranks([sum(step_ms)], world)[0]
+    counts = [r.clique_count for r in results]       # job totals (all_reduced)
+    kern_ms = [r.kernel_ms for r in results]         # max over ranks (device vector)
+    kmean = statistics.mean(kern_ms)
+    all_leaves = sum(counts)
     value = all_leaves / (total_ms * 1e-3)
+    launches = sum(r.launches for r in results)
 
-    # ---- e2e: host buffers through the public API, uploads inside ------------
-    off_h = torch.from_numpy(np.asarray(g.offsets)).pin_memory()
-    nbr_h = torch.from_numpy(np.asarray(g.neighbors_array)).pin_memory()
-    e2e_ms, h2d, d2h, e2e_leaves = [], 0, 0, 0
-    if world > 1:
-        torch.distributed.barrier()
-    for i in range(max(2, args.steps)):
-        flush.fill_(i)
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        gh = CsrGraph(g.n, off_h.numpy(), nbr_h.numpy())  # pinned host CSR, zero-copy view
-        r = step(gh)                       # wm_graph_create (H2D) + wm_run + D2H of results
-        engine.release_device_graph(gh)
-        torch.cuda.synchronize()
-        e2e_ms.append((time.perf_counter() - t0) * 1e3)
-        e2e_leaves += r.clique_count
-        h2d = off_h.numel() * 8 + nbr_h.numel() * 4 + r.extra["h2d_bytes"]
-        d2h = r.extra["d2h_bytes"]
-    e2e_total = sum(e2e_ms)
-    if world > 1:
-        t = torch.tensor([e2e_total], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        e2e_total = t.item()
-        c = torch.tensor([e2e_leaves], dtype=torch.int64, device="cuda")
-        torch.distributed.all_reduce(c)
-        e2e_leaves = int(c.item())
-    e2e_value = e2e_leaves / (e2e_total * 1e-3)
+    # ---- e2e: host buffers through the public API, uploads inside ----------
+    make_g, graph_bytes = _pinned_graph_factory(g)
+    e2e_ms, e2e_res = e2e_steps(make_g, step_on, max(2, args.steps), flush, world)
+    e2e_total = max_over_ranks([sum(e2e_ms)], world)[0]
+    e2e_value = sum(r.clique_count for r in e2e_res) / (e2e_total * 1e-3)
+    r_last = e2e_res[-1]
+    h2d = graph_bytes + r_last.extra["h2d_bytes"]
+    d2h = r_last.extra["d2h_bytes"]
 
     if rank != 0:
-        torch.distributed.barrier()
+        if world > 1:
+            torch.distributed.barrier()
+            torch.distributed.destroy_process_group()
         return 0
 
-    # ---- evidence (untimed): B_alg, LB off vs on, CPU baseline --------------
+    # ---- evidence (untimed, rank 0): B_alg, LB off vs on, motifs, CPU ---------
     peak, peak_src = load_peaks()
-    rb = run_clique(g, args.k, count_bytes=True, stream=stream, shard=(0, 1))
-    b_alg = rb.alg_bytes
-    achieved = b_alg / (kmean * 1e-3) / 1e9 if world == 1 else None
+    ncu = ncu_figures()
     extras = {}
-    if not args.no_extras:
-        rw = run_clique(g, args.k, mode="wc", stream=stream, shard=(0, 1))
-        ro = run_clique(g, args.k, mode="opt", balance_config=bc, stream=stream, shard=(0, 1))
+    achieved = None
+    b_alg = None
+    if world == 1:
+        rb = run_clique(g, args.k, count_bytes=True, stream=stream)
+        b_alg = rb.alg_bytes
+        achieved = b_alg / (kmean * 1e-3) / 1e9
+    clique_ncu = ncu.get("clique_enum_kernel", {})
+    issue = None
+    ci = clique_ncu.get("issue_k%d" % args.k)
+    if ci and clk:
+        # warp instructions per launch (ncu, same build) over the live kernel
+        # time, against 4 issue slots per SM per cycle at the sampled clock
+        peak_issue = 4 * 148 * clk["sm_mhz"] * 1e6
+        ach = ci["warp_inst_per_launch"] / (kmean * 1e-3)
+        issue = {"bound": "issue", "achieved": ach, "peak": peak_issue,
+                 "unit": "warp-inst/s", "frac": ach / peak_issue,
+                 "warp_inst_per_launch": ci["warp_inst_per_launch"],
+                 "ncu_issue_active": ci.get("issue_active"), "source": ci.get("source")}
+    if world == 1 and not args.no_extras:
+        rw = run_clique(g, args.k, mode="wc", stream=stream)
+        ro = run_clique(g, args.k, mode="opt", balance_config=bc, stream=stream)
         extras["load_balance"] = {
             "idle_warp_fraction_lb_off": rw.idle_warp_fraction,
             "idle_warp_fraction_lb_on": ro.idle_warp_fraction,
             "kernel_ms_lb_off": rw.kernel_ms, "kernel_ms_lb_on": ro.kernel_ms,
             "migrations": ro.migrations, "donations": ro.rebalance_count}
         extras["secondary"] = secondary_workloads(stream)
+    if world == 1 and not args.no_motif:
+        extras["motif"] = motif_block(args, stream, flush, gold, peak, peak_src, ncu)
     cpu = None
-    if world == 1 and args.cpu_budget > 0:
-        rate, lv, dt, rd, threads = cpu_sample(g, args.k, args.cpu_budget)
+    if world == 1 and not args.no_cpu:
+        rate, lv, dt, threads = cpu_clique_subset(g, args.k, args.ref_roots)
         cpu = {"value": rate, "unit": UNIT, "cores": threads, "kind": "port",
-               "sample": "reference clique_app pipeline (oracle/wm_oracle.c restatement, id order) "
-                         "on a seeded random root order of cfg3, time-boxed %.0f s: %d roots, %d "
-                         "cliques in %.1f s" % (args.cpu_budget, rd, lv, dt),
+               "sample": "reference clique_app pipeline (oracle/wm_oracle.c restatement of "
+                         "engine.py, id order) on the fixed seeded subset of %d cfg3 roots "
+                         "(the --impl reference step), run to completion: %d cliques in %.2f s"
+                         % (args.ref_roots, lv, dt),
                "cpu_model": cpu_model()}
-    r0 = results[0]
+        import oracle
+        t0 = time.perf_counter()
+        c_fast = oracle.clique_fast(g, args.k, threads=threads)
+        dt_fast = time.perf_counter() - t0
+        extras["cpu_context_strong"] = {
+            "value": c_fast / dt_fast, "unit": UNIT, "cores": threads,
+            "note": "NOT the reference algorithm: an independent degree-ordered kClist counter "
+                    "(oracle wmo_clique_fast) on the full cfg3 k=%d count, %.2f s; context for "
+                    "what a strong CPU code does" % (args.k, dt_fast),
+            "count_matches_golden": want is None or c_fast == want}
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int32/u64", "data": "synthetic",
         "config": workload_config(g, args.k, world),
-        "count_per_step": per_step_count,
-        "count_matches_golden": (want is None) or (per_step_count == want),
+        "count_per_step": counts[0],
+        "count_matches_golden": want is None or all(c == want for c in counts),
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / len(e2e_ms)},
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_total / len(e2e_ms),
+                "count_matches_golden": want is None or
+                all(r.clique_count == want for r in e2e_res)},
         "gpu_launches": launches,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": (achieved / peak) if achieved else None,
-                     "traffic": ncu_traffic(args.k), "peak_source": peak_src,
+                     "traffic": clique_ncu.get("k%d" % args.k), "peak_source": peak_src,
                      "kernel": "clique_enum_kernel<W=4>",
                      "alg_bytes_per_launch": b_alg,
-                     "alg_bytes_def": "4 B x sum over productive search-tree nodes of "
-                                      "deg+(last) in degree order (SURVEY 8(d))",
+                     "alg_bytes_def": "LIST-EQUIVALENT bytes: 4 B x sum over productive "
+                                      "search-tree nodes of deg+(last) in degree order (SURVEY "
+                                      "8(d)) - the adjacency a list-based extend reads; the "
+                                      "bitmap kernel never reads them, so frac > 1 is possible "
+                                      "and the kernel's real bound is issue (roofline_issue)",
                      "kernel_ms": kmean},
+        "roofline_issue": issue,
         "cpu_baseline": cpu,
         "clocks": clk,
-        "device": {"kernel_ms": kmean, "build_ms": r0.extra["build_ms"],
-                   "device_ms": r0.device_ms, "warps": r0.warps,
-                   "idle_warp_fraction": r0.idle_warp_fraction},
+        "collective": coll,
+        "device": {"kernel_ms": kmean, "build_ms": results[0].extra["build_ms"],
+                   "device_ms": results[0].device_ms, "warps": results[0].warps,
+                   "idle_warp_fraction": results[0].idle_warp_fraction},
     }
     line.update(extras)
     print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
     return 0
+
+
+def motif_block(args, stream, flush, gold, peak, peak_src, ncu):
+    """The k-motif half of the metric: each workload timed like the headline
+    (W warm-ups, K device-timed steps with L2 flush, histogram checked against
+    its golden every step), plus B_alg roofline, LB off/on idle fraction, e2e
+    through ``run_motifs`` from pinned host buffers and the CPU reference on a
+    fixed root subset."""
+    from paper_2212_04551_b200 import BalanceConfig, build_dictionary, run_motifs, synth
+    lb = BalanceConfig(threshold=1.0, poll_interval=2)
+    out = {}
+    for cfg, k, suffix, off_suffix in MOTIF_WORKLOADS:
+        g = synth.config_graph(cfg)
+        d = build_dictionary(k)
+        key = "k%d_s%d" % (k, suffix)
+        gk = gold.get(cfg, {}).get("motif_suffix", {}).get(key)
+        roots = (g.n - suffix, g.n)
+
+        def step_on(graph, **kw):
+            return run_motifs(graph, k, d, mode="opt", balance_config=lb, roots=roots,
+                              stream=stream, **kw)
+
+        for _ in range(args.warmup):
+            step_on(g)
+        step_ms, res, clk = timed_steps(lambda: step_on(g), args.steps, stream, flush, 1)
+        kms = statistics.mean(r.kernel_ms for r in res)
+        leaves = res[0].aggregated_total
+        rec = {
+            "workload": "%s k=%d motif histogram (motif_app), root suffix [n-%d, n) of %s"
+                        % (cfg, k, suffix, g.n),
+            "metric": "%d-motif subgraphs/s" % k, "unit": UNIT,
+            "value": leaves * len(res) / (sum(step_ms) * 1e-3),
+            "ms_per_step": sum(step_ms) / len(step_ms), "kernel_ms": kms,
+            "kernel_rate": leaves / (kms * 1e-3), "leaves_per_step": leaves,
+            "hist_matches_golden": None if gk is None else
+            all(r.pattern_counts == gk["hist"] for r in res),
+            "idle_warp_fraction_lb_on": res[0].idle_warp_fraction,
+            "gpu_launches": sum(r.launches for r in res), "clocks": clk}
+        # roofline: B_alg (instrumented pass, LB off) where that pass is short
+        traffic = ncu.get("motif_enum_kernel", {}).get("%s_%s" % (cfg, key))
+        if off_suffix == suffix:
+            rb = run_motifs(g, k, d, mode="wc", roots=roots, stream=stream, count_bytes=True)
+            ach = rb.alg_bytes / (kms * 1e-3) / 1e9
+            rec["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
+                               "frac": ach / peak, "traffic": traffic,
+                               "alg_bytes_per_launch": rb.alg_bytes, "peak_source": peak_src,
+                               "alg_bytes_def": "4 B x sum over productive search-tree nodes "
+                                                "of deg(last) (SURVEY 8(d))"}
+        else:
+            rec["roofline"] = {"bound": "hbm", "achieved": None, "peak": peak, "unit": "GB/s",
+                               "frac": None, "traffic": traffic,
+                               "note": "B_alg needs the LB-off instrumented pass, too long here"}
+        if off_suffix is not None:
+            rw = run_motifs(g, k, d, mode="wc", roots=(g.n - off_suffix, g.n), stream=stream)
+            ro = step_on(g) if off_suffix == suffix else run_motifs(
+                g, k, d, mode="opt", balance_config=lb, roots=(g.n - off_suffix, g.n),
+                stream=stream)
+            rec["load_balance"] = {"suffix": off_suffix,
+                                   "idle_warp_fraction_lb_off": rw.idle_warp_fraction,
+                                   "idle_warp_fraction_lb_on": ro.idle_warp_fraction,
+                                   "kernel_ms_lb_off": rw.kernel_ms,
+                                   "kernel_ms_lb_on": ro.kernel_ms,
+                                   "migrations": ro.migrations, "donations": ro.rebalance_count}
+        make_g, graph_bytes = _pinned_graph_factory(g)
+        e_ms, e_res = e2e_steps(make_g, step_on, 2, flush, 1)
+        rec["e2e"] = {"value": sum(r.aggregated_total for r in e_res) / (sum(e_ms) * 1e-3),
+                      "unit": UNIT, "ms_per_step": sum(e_ms) / len(e_ms),
+                      "h2d_bytes_per_step": graph_bytes + e_res[-1].extra["h2d_bytes"],
+                      "d2h_bytes_per_step": e_res[-1].extra["d2h_bytes"],
+                      "note": "fresh graph per step: CSR upload + validation + edge-hash build "
+                              "+ run + histogram read-back",
+                      "hist_matches_golden": None if gk is None else
+                      all(r.pattern_counts == gk["hist"] for r in e_res)}
+        if not args.no_cpu:
+            nr = MOTIF_CPU_ROOTS.get((cfg, k), 1024)
+            rate, lv, dt, threads = cpu_motif_subset(g, k, suffix, nr)
+            rec["cpu_baseline"] = {
+                "value": rate, "unit": UNIT, "cores": threads, "kind": "port",
+                "sample": "reference motif_app pipeline (oracle/wm_oracle.c restatement) on a "
+                          "fixed seeded subset of %d of the suffix's %d roots, run to "
+                          "completion: %d subgraphs in %.2f s" % (nr, suffix, lv, dt),
+                "cpu_model": cpu_model()}
+        out["%s_%s" % (cfg, key)] = rec
+    return out
 
 
 def secondary_workloads(stream):
     """configs 1 and 2 (exact, tiny) for the record; not the headline."""
-    from paper_2212_04551_b200 import build_dictionary, run_clique, run_motifs, synth
+    from paper_2212_04551_b200 import (BalanceConfig, build_dictionary, run_clique, run_motifs,
+                                       synth)
     out = {}
     g1 = synth.config_graph("cfg1")
     for k in (3, 4):
-        r = run_clique(g1, k, stream=stream, shard=(0, 1))
+        r = run_clique(g1, k, stream=stream)
         out["cfg1_clique_k%d" % k] = {"count": r.clique_count, "kernel_ms": r.kernel_ms}
-    from paper_2212_04551_b200 import BalanceConfig
     g2 = synth.config_graph("cfg2")
     lb = BalanceConfig(threshold=1.0, poll_interval=2)
     for k in (4, 6):
         for mode, kw in (("wc", {}), ("opt", {"balance_config": lb})):
-            run_motifs(g2, k, build_dictionary(k), mode=mode, stream=stream, shard=(0, 1), **kw)
-            r = run_motifs(g2, k, build_dictionary(k), mode=mode, stream=stream, shard=(0, 1), **kw)
+            run_motifs(g2, k, build_dictionary(k), mode=mode, stream=stream, **kw)
+            r = run_motifs(g2, k, build_dictionary(k), mode=mode, stream=stream, **kw)
             out["cfg2_motif_k%d%s" % (k, "" if mode == "wc" else "_opt")] = {
                 "leaves": r.aggregated_total, "kernel_ms": r.kernel_ms,
                 "subgraphs_per_s": r.subgraphs_per_second, "hist_head": r.pattern_counts[:6],

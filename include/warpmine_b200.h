@@ -7,8 +7,10 @@
  *         -> RunResult                 (pkg/src/warpmine/engine.py:781-843)
  *
  * Plain pointers and sizes only.  Host pointers are borrowed for the duration
- * of the call; device memory is owned by the library.  Calls are blocking and
- * not re-entrant per graph handle.  Status codes map onto the reference's
+ * of the call; device memory is owned by the library.  Calls are blocking;
+ * the library's per-device scratch is held for the whole of each call, so
+ * concurrent calls on one device are serialised (a call from inside a listing
+ * sink callback is refused with WM_EINVAL).  Status codes map onto the reference's
  * exception taxonomy (pkg/src/warpmine/errors.py:4-31) in
  * paper_2212_04551_b200/_native.py:
  *
@@ -31,7 +33,7 @@
 extern "C" {
 #endif
 
-#define WM_ABI_VERSION 1
+#define WM_ABI_VERSION 2
 
 #define WM_OK 0
 #define WM_EINVAL (-1)
@@ -100,7 +102,40 @@ typedef struct {
   int warps_per_block;      /* 0 = auto */
   int blocks_per_sm;        /* 0 = auto (occupancy) */
   void *stream;             /* cudaStream_t to run on; NULL = library stream */
+  uint64_t *reduce_out;     /* optional DEVICE buffer of wm_reduce_words() u64:
+                               the run's result vector, written on `stream`
+                               (layout below) so one collective on that stream
+                               sums every rank's results (aggregate.py:39-55)
+                               with no host round trip.  NULL = not written. */
 } wm_cfg;
+
+/* Device result vector (wm_cfg.reduce_out), u64 words:
+ *   [WM_RED_CLIQUES] clique_count   [WM_RED_LEAVES] leaves (aggregated_total)
+ *   [WM_RED_ALG_BYTES] B_alg        [WM_RED_MIGRATIONS] migrations
+ *   [WM_RED_DONATIONS] rebalance_count  [WM_RED_TASKS] root tasks
+ *   [WM_RED_RECORDS] [WM_RED_CHECKSUM] listing (0 for wm_run)
+ *   [WM_RED_HIST .. +pattern_count) pattern histogram
+ *   then shard_count slots of WM_RED_SLOT_WORDS: slot shard_rank holds this
+ *   rank's kernel_ms, device_ms, idle_warp_fraction, idle_warp_fraction_tail
+ *   as IEEE-754 double bit patterns; other slots are 0.
+ * Every word is a sum over ranks: counters add (mod 2^64), and each timing
+ * slot has exactly one non-zero contributor, so ncclAllReduce(ncclUint64,
+ * ncclSum) over the whole vector leaves every rank's timings intact for a
+ * max on the host. */
+#define WM_RED_CLIQUES 0
+#define WM_RED_LEAVES 1
+#define WM_RED_ALG_BYTES 2
+#define WM_RED_MIGRATIONS 3
+#define WM_RED_DONATIONS 4
+#define WM_RED_TASKS 5
+#define WM_RED_RECORDS 6
+#define WM_RED_CHECKSUM 7
+#define WM_RED_HIST 8
+#define WM_RED_SLOT_WORDS 4
+
+/* words of the reduce_out vector for `pattern_count` patterns (0 for the
+ * counter aggregator) and `shard_count` ranks */
+uint64_t wm_reduce_words(uint32_t pattern_count, int shard_count);
 
 /* RunResult (engine.py:747-762) plus device evidence. */
 typedef struct {
@@ -206,10 +241,15 @@ void wm_csr_free(wm_csr_out *out);
 int wm_dictionary_build(int k, uint32_t *table_out, uint64_t *bitmaps_out, uint32_t bitmaps_cap,
                         uint32_t *pattern_count);
 
-/* Upload a CSR graph to the current device (cudaSetDevice beforehand). */
+/* Upload a CSR graph to the current device (cudaSetDevice beforehand).
+ * The CsrGraph contract (graph.py:122-133) is checked on the device after the
+ * upload: offsets span nnz and never decrease, every neighbour id is in
+ * [0, n), rows are strictly ascending, there are no self-loops and every edge
+ * is symmetric.  A violation returns WM_EINVAL naming the first offending
+ * vertex/edge, in the reference's wording. */
 int wm_graph_create(const wm_csr *csr, void **graph);
 
-/* Same, from device-resident arrays (copied device-to-device). */
+/* Same, from device-resident arrays (copied device-to-device; same checks). */
 int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
                            const int32_t *d_neighbors, void **graph);
 

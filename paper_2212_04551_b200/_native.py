@@ -28,7 +28,12 @@ WM_ORDER_ID, WM_ORDER_DEGREE = 0, 1
 
 EXPORTED = ("wm_graph_create", "wm_graph_create_device", "wm_run", "wm_run_listing",
             "wm_graph_destroy", "wm_last_error", "wm_abi_version", "wm_csr_build",
-            "wm_edge_list_parse", "wm_csr_free", "wm_dictionary_build")
+            "wm_edge_list_parse", "wm_csr_free", "wm_dictionary_build", "wm_reduce_words")
+ABI_VERSION = 2
+# device result vector layout (wm_cfg.reduce_out, include/warpmine_b200.h)
+WM_RED_CLIQUES, WM_RED_LEAVES, WM_RED_ALG_BYTES, WM_RED_MIGRATIONS, WM_RED_DONATIONS, \
+    WM_RED_TASKS, WM_RED_RECORDS, WM_RED_CHECKSUM, WM_RED_HIST = range(9)
+WM_RED_SLOT_WORDS = 4
 
 
 class WmCsr(ctypes.Structure):
@@ -51,7 +56,8 @@ class WmCfg(ctypes.Structure):
                 ("root_end", ctypes.c_int64), ("shard_rank", ctypes.c_int),
                 ("shard_count", ctypes.c_int), ("order", ctypes.c_int),
                 ("count_bytes", ctypes.c_int), ("warps_per_block", ctypes.c_int),
-                ("blocks_per_sm", ctypes.c_int), ("stream", ctypes.c_void_p)]
+                ("blocks_per_sm", ctypes.c_int), ("stream", ctypes.c_void_p),
+                ("reduce_out", ctypes.c_void_p)]
 
 
 class WmResult(ctypes.Structure):
@@ -129,6 +135,11 @@ def load():
     L.wm_last_error.restype = ctypes.c_char_p
     L.wm_abi_version.argtypes = []
     L.wm_abi_version.restype = ctypes.c_int
+    L.wm_reduce_words.argtypes = [ctypes.c_uint32, ctypes.c_int]
+    L.wm_reduce_words.restype = ctypes.c_uint64
+    if L.wm_abi_version() != ABI_VERSION:
+        raise ImportError("libwm_b200.so ABI %d, expected %d: rebuild it"
+                          % (L.wm_abi_version(), ABI_VERSION))
     _LIB = L
     return L
 

@@ -103,6 +103,164 @@ void finish_lb_stats(const LbState &h, wm_result *res) {
   res->peak_ext = h.peak_ext;
 }
 
+// ---------------------------------------------------------------------------
+// device result vector (wm_cfg.reduce_out, include/warpmine_b200.h): every
+// word is a sum over runs and ranks, so packing adds into it
+
+__global__ void red_pack_kernel(unsigned long long *__restrict__ out,
+                                const unsigned long long *__restrict__ ctr, int is_clique,
+                                int alg_bytes, int add_tasks, const LbState *__restrict__ lbs,
+                                int nlb, const unsigned long long *__restrict__ hist, uint32_t P) {
+  if (threadIdx.x == 0) {
+    const unsigned long long c = ctr[0];
+    if (is_clique) out[WM_RED_CLIQUES] += c;
+    out[WM_RED_LEAVES] += c;
+    if (alg_bytes) out[WM_RED_ALG_BYTES] += ctr[1];
+    if (add_tasks) out[WM_RED_TASKS] += ctr[2];
+    for (int i = 0; i < nlb; ++i) {
+      out[WM_RED_MIGRATIONS] += lbs[i].migrations;
+      out[WM_RED_DONATIONS] += lbs[i].donation_polls;
+    }
+  }
+  if (hist)
+    for (uint32_t i = threadIdx.x; i < P; i += blockDim.x) out[WM_RED_HIST + i] += hist[i];
+}
+
+// out[i] += v[i - idx] for four host-known words (timing slots, task counts)
+__global__ void red_add_kernel(unsigned long long *out, unsigned long long a,
+                               unsigned long long b, unsigned long long c, unsigned long long d) {
+  if (threadIdx.x == 0) {
+    out[0] += a;
+    out[1] += b;
+    out[2] += c;
+    out[3] += d;
+  }
+}
+
+// the 2-cliques of a wide root's induced subgraph are its edges: nnz / 2
+__global__ void red_edges_kernel(unsigned long long *out, const int64_t *nnz) {
+  if (threadIdx.x == 0) {
+    const unsigned long long e = (unsigned long long)(*nnz) / 2ull;
+    out[WM_RED_CLIQUES] += e;
+    out[WM_RED_LEAVES] += e;
+  }
+}
+
+int red_pack(const wm_cfg *cfg, cudaStream_t s, const unsigned long long *ctr, bool is_clique,
+             bool alg_bytes, bool add_tasks, const LbState *lbs, int nlb,
+             const unsigned long long *hist, uint32_t P) {
+  if (!cfg->reduce_out) return WM_OK;
+  red_pack_kernel<<<1, 256, 0, s>>>(reinterpret_cast<unsigned long long *>(cfg->reduce_out),
+                                    ctr, is_clique, alg_bytes, add_tasks, lbs, nlb, hist, P);
+  WM_CUDA(cudaGetLastError());
+  return WM_OK;
+}
+
+int red_add(const wm_cfg *cfg, cudaStream_t s, uint64_t idx, unsigned long long a,
+            unsigned long long b, unsigned long long c, unsigned long long d) {
+  if (!cfg->reduce_out) return WM_OK;
+  red_add_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned long long *>(cfg->reduce_out) + idx,
+                                  a, b, c, d);
+  WM_CUDA(cudaGetLastError());
+  return WM_OK;
+}
+
+int red_edges(const wm_cfg *cfg, cudaStream_t s, const int64_t *nnz) {
+  if (!cfg->reduce_out) return WM_OK;
+  red_edges_kernel<<<1, 32, 0, s>>>(reinterpret_cast<unsigned long long *>(cfg->reduce_out), nnz);
+  WM_CUDA(cudaGetLastError());
+  return WM_OK;
+}
+
+// ---------------------------------------------------------------------------
+// CsrGraph.validate (graph.py:122-133) on the device, warp per vertex.  The
+// first violation in the reference's check order wins: vertex u ascending,
+// then per u: range/offsets, strictly ascending, self-loop, symmetry (first v
+// in row order).  Key = u << 33 | code << 31 | detail; atomicMin.
+enum : unsigned long long { kCsrRange = 0, kCsrAscend = 1, kCsrLoop = 2, kCsrSym = 3 };
+
+__global__ void csr_check_kernel(int64_t n, int64_t nnz, const int64_t *__restrict__ off,
+                                 const int32_t *__restrict__ nbr,
+                                 unsigned long long *__restrict__ bad) {
+  const int lane = lane_id();
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
+    int64_t b = off[u], e = off[u + 1];
+    unsigned long long key = ~0ull;
+    if (e < b || b < 0 || e > nnz) {
+      key = ((unsigned long long)u << 33) | (kCsrRange << 31);  // detail 0: offsets
+    } else {
+      for (int64_t p0 = b; p0 < e; p0 += 32) {
+        const int64_t p = p0 + lane;
+        unsigned long long k = ~0ull;
+        if (p < e) {
+          const int32_t v = nbr[p];
+          const unsigned long long det = (unsigned long long)(p - b + 1) & 0x7FFFFFFFull;
+          if (v < 0 || v >= n) {
+            k = ((unsigned long long)u << 33) | (kCsrRange << 31) | det;
+          } else if (p > b && nbr[p - 1] >= v) {
+            k = ((unsigned long long)u << 33) | (kCsrAscend << 31);
+          } else if (v == u) {
+            k = ((unsigned long long)u << 33) | (kCsrLoop << 31);
+          } else {
+            int64_t lo = off[v], hi = off[v + 1];
+            if (lo < 0) lo = 0;
+            if (hi > nnz) hi = nnz;
+            bool found = false;
+            while (lo < hi) {
+              const int64_t mid = (lo + hi) >> 1;
+              const int32_t y = nbr[mid];
+              if (y == (int32_t)u) { found = true; break; }
+              if (y < (int32_t)u) lo = mid + 1; else hi = mid;
+            }
+            if (!found) k = ((unsigned long long)u << 33) | (kCsrSym << 31) | (unsigned long long)v;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const unsigned long long y = __shfl_xor_sync(0xffffffffu, k, o);
+          k = y < k ? y : k;
+        }
+        key = k < key ? k : key;
+        if (key != ~0ull) break;  // later positions of this row cannot win
+      }
+    }
+    if (lane == 0 && key != ~0ull) atomicMin(bad, key);
+  }
+}
+
+// runs the check on stream s (graph arrays already on the device); host
+// offsets bounds are checked by the caller
+static int csr_validate(Graph *g, cudaStream_t s) {
+  int st = g->ws->counters.ensure(sizeof(unsigned long long) * 64);
+  if (st) return st;
+  unsigned long long *bad = g->ws->counters.as<unsigned long long>() + 63;
+  WM_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+  const int64_t want = (g->n * 32 + 255) / 256;
+  const int blocks = (int)(want < (int64_t)g->num_sms * 16 ? want : (int64_t)g->num_sms * 16);
+  csr_check_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(g->n, g->nnz, g->offsets,
+                                                           g->neighbors, bad);
+  WM_CUDA(cudaGetLastError());
+  unsigned long long h = ~0ull;
+  WM_CUDA(cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, s));
+  WM_CUDA(cudaStreamSynchronize(s));
+  if (h == ~0ull) return WM_OK;
+  const long long u = (long long)(h >> 33);
+  const unsigned long long code = (h >> 31) & 3ull, det = h & 0x7FFFFFFFull;
+  switch (code) {
+    case kCsrRange:
+      if (det == 0) return fail(WM_EINVAL, "offsets must be non-decreasing (vertex %lld)", u);
+      return fail(WM_EINVAL, "neighbour #%llu of vertex %lld is outside [0, %lld)", det - 1, u,
+                  (long long)g->n);
+    case kCsrAscend:
+      return fail(WM_EINVAL, "adjacency of %lld not strictly ascending", u);
+    case kCsrLoop:
+      return fail(WM_EINVAL, "self-loop at %lld", u);
+    default:
+      return fail(WM_EINVAL, "edge (%lld,%llu) not symmetric", u, det);
+  }
+}
+
 static std::mutex g_ws_mu;
 static Workspace *g_ws[64];
 
@@ -182,6 +340,8 @@ int wm_graph_create(const wm_csr *csr, void **out) {
   Graph *g = new Graph();
   int st = graph_init(g);
   if (st) { delete g; return st; }
+  WsLock lk(g->ws);
+  if ((st = lk.status())) { delete g; return st; }
   g->n = csr->n;
   g->nnz = csr->nnz;
   g->max_degree = md;
@@ -197,6 +357,10 @@ int wm_graph_create(const wm_csr *csr, void **out) {
   if (e != cudaSuccess) {
     wm_graph_destroy(g);
     return fail(WM_ECUDA, "graph upload failed: %s", cudaGetErrorString(e));
+  }
+  if ((st = csr_validate(g, s))) {
+    wm_graph_destroy(g);
+    return st;
   }
   *out = g;
   return WM_OK;
@@ -224,9 +388,12 @@ int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
   if (!out || !d_offsets || n < 1) return fail(WM_EINVAL, "bad device graph arguments");
   if (n >= (1ll << 31) - 1) return fail(WM_EINVAL, "n=%lld exceeds int32 vertex ids",
                                         (long long)n);
+  if (nnz < 0) return fail(WM_EINVAL, "negative nnz");
   Graph *g = new Graph();
   int st = graph_init(g);
   if (st) { delete g; return st; }
+  WsLock lk(g->ws);
+  if ((st = lk.status())) { delete g; return st; }
   g->n = n;
   g->nnz = nnz;
   cudaStream_t s = g->ws->own_stream;
@@ -250,13 +417,26 @@ int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
       e = cudaGetLastError();
     }
     unsigned long long h = 0;
+    int64_t ends[2] = {0, 0};
     if (e == cudaSuccess) e = cudaMemcpyAsync(&h, md, sizeof h, cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&ends[0], g->offsets, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(&ends[1], g->offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
     if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     g->max_degree = (int64_t)h;
+    if (e == cudaSuccess && (ends[0] != 0 || ends[1] != nnz)) {
+      wm_graph_destroy(g);
+      return fail(WM_EINVAL, "offsets do not span nnz=%lld", (long long)nnz);
+    }
   }
   if (e != cudaSuccess) {
     wm_graph_destroy(g);
     return fail(WM_ECUDA, "device graph copy failed: %s", cudaGetErrorString(e));
+  }
+  if ((st = csr_validate(g, s))) {
+    wm_graph_destroy(g);
+    return st;
   }
   *out = g;
   return WM_OK;
@@ -296,11 +476,44 @@ static int check_run_args(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_res
   return WM_OK;
 }
 
+uint64_t wm_reduce_words(uint32_t pattern_count, int shard_count) {
+  return (uint64_t)WM_RED_HIST + pattern_count +
+         (uint64_t)WM_RED_SLOT_WORDS * (uint64_t)(shard_count > 0 ? shard_count : 1);
+}
+
+static unsigned long long dbits(double x) {
+  unsigned long long u;
+  memcpy(&u, &x, sizeof u);
+  return u;
+}
+
+static int wm_run_locked(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res);
+
 int wm_run(void *gp, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
   g_last_error.clear();
   Graph *g = static_cast<Graph *>(gp);
   int st = check_run_args(g, app, cfg, res);
   if (st) return st;
+  WsLock lk(g->ws);
+  if ((st = lk.status())) return st;
+  cudaStream_t s = cfg->stream ? static_cast<cudaStream_t>(cfg->stream) : g->ws->own_stream;
+  const uint32_t P = app->aggregator == WM_AGG_PATTERN ? app->pattern_count : 0;
+  if (cfg->reduce_out) {
+    if (reinterpret_cast<uintptr_t>(cfg->reduce_out) & 7u)
+      return fail(WM_EINVAL, "reduce_out must be 8-byte aligned");
+    WM_CUDA(cudaMemsetAsync(cfg->reduce_out, 0,
+                            sizeof(uint64_t) * wm_reduce_words(P, cfg->shard_count), s));
+  }
+  st = wm_run_locked(g, app, cfg, res);
+  if (st == WM_OK && cfg->reduce_out)
+    st = red_add(cfg, s, (uint64_t)WM_RED_HIST + P +
+                             (uint64_t)WM_RED_SLOT_WORDS * (uint64_t)cfg->shard_rank,
+                 dbits(res->kernel_ms), dbits(res->device_ms), dbits(res->idle_warp_fraction),
+                 dbits(res->idle_warp_fraction_tail));
+  return st;
+}
+
+static int wm_run_locked(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res) {
   const bool clique = app->aggregator == WM_AGG_COUNTER && !app->extend_all &&
                       (app->filters & WM_F_CLIQUE) && (app->filters & WM_F_LOWER) &&
                       !(app->filters & WM_F_CANONICAL);
@@ -338,6 +551,11 @@ int wm_run_listing(void *gp, const wm_app *app, const wm_cfg *cfg, wm_listing *l
   int st = check_run_args(g, app, cfg, res);
   if (st) return st;
   if (!lst) return fail(WM_EINVAL, "null listing");
+  if (cfg->reduce_out)
+    return fail(WM_EINVAL, "listing results (records, checksum) are produced on the host; "
+                           "reduce_out is not supported for wm_run_listing");
+  WsLock lk(g->ws);
+  if ((st = lk.status())) return st;
   // listing_app (apps.py:61-67): extend(0,len), canonical, store
   if (!(app->aggregator == WM_AGG_STORE && app->extend_all && app->genedges &&
         app->filters == WM_F_CANONICAL))

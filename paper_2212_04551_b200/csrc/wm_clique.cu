@@ -1397,7 +1397,7 @@ __global__ void induced_fill_kernel(int d, const int32_t *__restrict__ M,
 }
 
 static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res,
-                           cudaStream_t s, std::vector<std::vector<int32_t>> *wide);
+                           cudaStream_t s, std::vector<std::vector<int32_t>> *wide, bool top);
 
 // count the (k-1)-cliques of G[M] for every wide root's member list and add
 // them (and the nested runs' statistics) into res
@@ -1436,6 +1436,7 @@ static int clique_wide_roots(Graph *g, const wm_app *app, const wm_cfg *cfg,
     if (app->k - 1 == 2) {
       res->clique_count += (uint64_t)nnz / 2;  // 2-cliques of G[M]: its edges
       res->leaves += (uint64_t)nnz / 2;
+      st = red_edges(cfg, s, doff + d);
     } else if (nnz > 0) {
       WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&dnbr), sizeof(int32_t) * nnz,
                                       g->ws->pool, s));
@@ -1459,7 +1460,7 @@ static int clique_wide_roots(Graph *g, const wm_app *app, const wm_cfg *cfg,
       sc.order = WM_ORDER_DEGREE;
       wm_result r = {};
       std::vector<std::vector<int32_t>> nested;
-      st = run_clique_impl(&sub, &sa, &sc, &r, s, &nested);
+      st = run_clique_impl(&sub, &sa, &sc, &r, s, &nested, false);
       if (st == WM_OK && !nested.empty()) st = clique_wide_roots(&sub, &sa, &sc, nested, &r, s);
       res->clique_count += r.clique_count;
       res->leaves += r.leaves;
@@ -1488,13 +1489,15 @@ static int clique_wide_roots(Graph *g, const wm_app *app, const wm_cfg *cfg,
 
 int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s) {
   std::vector<std::vector<int32_t>> wide;
-  int st = run_clique_impl(g, app, cfg, res, s, &wide);
+  int st = run_clique_impl(g, app, cfg, res, s, &wide, true);
   if (st || wide.empty()) return st;
+  // each top-level wide root is one task of this shard (nested runs add none)
+  if ((st = red_add(cfg, s, WM_RED_TASKS, (unsigned long long)wide.size(), 0, 0, 0))) return st;
   return clique_wide_roots(g, app, cfg, wide, res, s);
 }
 
 static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res,
-                           cudaStream_t s, std::vector<std::vector<int32_t>> *wide) {
+                           cudaStream_t s, std::vector<std::vector<int32_t>> *wide, bool top) {
   PhaseTimer pt(s);
   const int64_t n = g->n;
   const int k = app->k;
@@ -1586,6 +1589,7 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
     WM_CUDA(cudaMemsetAsync(ctr + 16, 0, sizeof(unsigned long long), s));
     int st2 = run_clique_dfs(g, cfg, k, ntask, key0 ? (int)key0 - 1 : 1, res, s, kb, k1);
     if (st2) return st2;
+    if ((st2 = red_pack(cfg, s, ctr, true, false, top, nullptr, 0, nullptr, 0))) return st2;
     unsigned long long hc[8];
     WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
     WM_CUDA(cudaEventRecord(e1, s));
@@ -1761,6 +1765,7 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   }
   WM_CUDA(cudaEventRecord(k1, s));
   pt.mark("enumerate");
+  if ((st = red_pack(cfg, s, ctr, true, bytes, top, lbs, launched, nullptr, 0))) return st;
   unsigned long long hc[8];
   WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
   LbState hl[8];

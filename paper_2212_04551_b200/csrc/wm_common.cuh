@@ -21,9 +21,12 @@
 //   without stopping and relaunching the kernel.
 #pragma once
 
+#include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <mutex>
 #include <string>
+#include <thread>
 #include <cuda_runtime.h>
 #include <cuda/atomic>
 
@@ -363,9 +366,13 @@ struct DeviceBuffer {
 
 // Per-device scratch, shared by every graph handle on that device: grow-only
 // buffers reused across runs and across graphs, so a fresh upload (the e2e
-// path) pays no cudaMalloc/cudaFree.  Calls are not re-entrant per device
-// (header contract); `mu` serialises concurrent callers.
+// path) pays no cudaMalloc/cudaFree.  Every C-ABI entry point that touches it
+// holds `mu` for the whole call (WsLock), so concurrent callers on one device
+// (ctypes releases the GIL) are serialised; a nested call from the same
+// thread (a listing sink calling back into the library) is refused.
 struct Workspace {
+  std::mutex mu;
+  std::atomic<std::thread::id> owner{};
   int device = 0;
   int num_sms = 0;
   cudaStream_t own_stream = nullptr;
@@ -378,6 +385,39 @@ struct Workspace {
 
 // returns the workspace of the current device (created on first use)
 int workspace_get(Workspace **out);
+
+// Scoped hold of a workspace for one C-ABI call.  status() is WM_EINVAL when
+// the calling thread already holds it (re-entry from a sink callback).
+class WsLock {
+ public:
+  explicit WsLock(Workspace *w) : w_(w) {
+    if (!w_) return;
+    if (w_->owner.load() == std::this_thread::get_id()) {
+      reentrant_ = true;
+      return;
+    }
+    w_->mu.lock();
+    w_->owner.store(std::this_thread::get_id());
+    held_ = true;
+  }
+  ~WsLock() {
+    if (held_) {
+      w_->owner.store(std::thread::id());
+      w_->mu.unlock();
+    }
+  }
+  int status() const {
+    return reentrant_ ? fail(WM_EINVAL, "re-entrant call into libwm_b200 on device %d (a "
+                                        "listing sink may not start another run)", w_->device)
+                      : WM_OK;
+  }
+  WsLock(const WsLock &) = delete;
+  WsLock &operator=(const WsLock &) = delete;
+
+ private:
+  Workspace *w_ = nullptr;
+  bool held_ = false, reentrant_ = false;
+};
 
 struct Graph {
   int64_t n = 0, nnz = 0;
@@ -411,6 +451,18 @@ int lb_prepare(Graph *g, LbState *lb, int warps, uint32_t words, LbShared *out, 
 int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s);
 int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s,
               wm_listing *lst = nullptr);
+
+// device result vector (wm_cfg.reduce_out; no-ops when it is NULL):
+// adds one run's counters (ctr[0] count/leaves, ctr[1] B_alg, ctr[2] tasks),
+// its balancer statistics and histogram on stream s
+int red_pack(const wm_cfg *cfg, cudaStream_t s, const unsigned long long *ctr, bool is_clique,
+             bool alg_bytes, bool add_tasks, const LbState *lbs, int nlb,
+             const unsigned long long *hist, uint32_t P);
+// adds four host-known words at reduce_out[idx .. idx+4)
+int red_add(const wm_cfg *cfg, cudaStream_t s, uint64_t idx, unsigned long long a,
+            unsigned long long b, unsigned long long c, unsigned long long d);
+// adds *nnz / 2 cliques and leaves (device-resident edge count)
+int red_edges(const wm_cfg *cfg, cudaStream_t s, const int64_t *nnz);
 
 // fills the idle fractions and LB stats of `res` from a device LbState copy
 void finish_lb_stats(const LbState &h, wm_result *res);

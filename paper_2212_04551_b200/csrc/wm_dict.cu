@@ -115,6 +115,8 @@ extern "C" int wm_dictionary_build(int k, uint32_t *table_out, uint64_t *bitmaps
   Workspace *ws = nullptr;
   int st = workspace_get(&ws);
   if (st) return st;
+  WsLock lk(ws);
+  if ((st = lk.status())) return st;
   cudaStream_t s = ws->own_stream;
   const int nbits = stored_bits_of(k);
   const unsigned long long size = 1ull << nbits;

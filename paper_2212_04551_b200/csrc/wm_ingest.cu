@@ -405,6 +405,8 @@ int wm_csr_build(int64_t n, const int64_t *src, const int64_t *dst, int64_t m,
   Workspace *ws = nullptr;
   int st = workspace_get(&ws);
   if (st) return st;
+  WsLock lk(ws);
+  if ((st = lk.status())) return st;
   cudaStream_t s = ws->own_stream;
   cudaEvent_t a = ws->ev[4], b = ws->ev[5];
   WM_CUDA(cudaEventRecord(a, s));
@@ -432,6 +434,8 @@ int wm_edge_list_parse(const char *text, uint64_t len, wm_csr_out *out) {
   Workspace *ws = nullptr;
   int st = workspace_get(&ws);
   if (st) return st;
+  WsLock lk(ws);
+  if ((st = lk.status())) return st;
   cudaStream_t s = ws->own_stream;
   cudaEvent_t a = ws->ev[4], b = ws->ev[5];
   WM_CUDA(cudaEventRecord(a, s));

@@ -1186,15 +1186,20 @@ static int drain_listing(HostRing *h, unsigned long long cap, uint32_t stride, i
         unsigned long long head = 0;
         WM_CUDA(cudaMemcpyAsync(&head, dhead, sizeof head, cudaMemcpyDeviceToHost, cs));
         WM_CUDA(cudaStreamSynchronize(cs));
-        if (head > tail) {
-          // the block at the tail is the last, partial one (head - tail < G)
-          const unsigned long long n = head - tail;
+        // several blocks may have completed between the last counter poll
+        // and the event query, so [tail, head) can span the ring's end (and
+        // exceed one block): drain it in pieces that stop at the wrap (the
+        // staging buffer holds a whole ring, cap records)
+        while (head > tail && !failed) {
+          const unsigned long long to_end = cap - (tail & mask);
+          unsigned long long n = head - tail;
+          if (n > to_end) n = to_end;
           WM_CUDA(cudaMemcpyAsync(h->stage, dring + (tail & mask) * stride,
                                   sizeof(uint32_t) * stride * n, cudaMemcpyDeviceToHost, cs));
           WM_CUDA(cudaStreamSynchronize(cs));
           if (consume(h->stage, n, stride, k, lst, sum)) emitted += n;
           else failed = true;
-          tail = head;
+          tail += n;
         }
       }
       break;
@@ -1374,6 +1379,9 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
                              a.ring.blockdone, block_shift, a.ring.head, a.ring.ctl);
     if (drain_st == WM_ECUDA) return drain_st;
   }
+  if (!lst && (st = red_pack(cfg, s, ctr, false, bytes, true, a.L.lb, a.ntasks ? 1 : 0,
+                             g->ws->hist.as<unsigned long long>(), app->pattern_count)))
+    return st;
   unsigned long long hc[8];
   WM_CUDA(cudaMemcpyAsync(hc, ctr, sizeof hc, cudaMemcpyDeviceToHost, s));
 #if WM_MOTIF_PROF

@@ -11,14 +11,26 @@ pipelines other than the built-in clique/motif ones raise ValueError.
 
 Extra keyword arguments (all optional, B200-only):
   roots        (begin, end) root-id range; ``None`` = all vertices
-               (engine.py:187).  Root-suffix runs enumerate exactly the
-               subgraphs whose minimum vertex id is >= begin.
+               (engine.py:187).  A root is the first vertex of a
+               traversal: for motifs (and listing) the lowest id of the
+               subgraph (canonical rule, canon.py:190-210); for cliques the
+               lowest vertex in the clique ``order`` — so a suffix
+               ``(b, n)`` enumerates exactly the subgraphs of the induced
+               subgraph on ids >= b for motifs, and for cliques only with
+               ``order="id"`` (under "degree" the suffix selects cliques
+               by their lowest-(degree, id) member).
   order        "degree" (default) or "id": orientation of the clique DAG.
                Counts are order-invariant; "id" reproduces the reference
                tree exactly (and its B_alg).
   count_bytes  also compute B_alg — an instrumented pass.
   shard        (rank, count): process this rank's cyclic share of the
-               cost-sorted root tasks (see ``parallel.py``).
+               cost-sorted root tasks (see ``parallel.py``); ``"auto"`` =
+               (rank, world) of the initialised torch.distributed group.
+               Default (0, 1): a plain call never becomes a collective.
+  reduce       with count > 1, combine the ranks' results (default True):
+               ``wm_run`` writes its result vector into a device buffer on
+               the run's stream and ONE all_reduce(SUM) over it (NCCL on
+               that stream) yields the job totals on every rank.
   stream       a ``torch.cuda.Stream`` (or raw cudaStream_t int) to run on.
 """
 
@@ -278,8 +290,13 @@ def run(g: CsrGraph, app: Application, *, mode: str = "wc", warps: int = None,
             raise ValueError("root range %r outside 0..%d" % ((rb, re), g.n))
         cfg.root_begin, cfg.root_end = rb, re
     if shard is None:
+        shard = (0, 1)
+    elif shard == "auto":
         from . import parallel
         shard = parallel.default_shard()
+    shard = (int(shard[0]), int(shard[1]))
+    if not (shard[1] >= 1 and 0 <= shard[0] < shard[1]):
+        raise ValueError("bad shard %r" % (shard,))
     cfg.shard_rank, cfg.shard_count = shard
     cfg.order = _native.WM_ORDER_ID if order == "id" else _native.WM_ORDER_DEGREE
     cfg.count_bytes = int(count_bytes)
@@ -294,6 +311,12 @@ def run(g: CsrGraph, app: Application, *, mode: str = "wc", warps: int = None,
     if app.aggregator == "pattern":
         hist = np.zeros(app.dictionary.pattern_count, dtype=np.uint64)
         res.pattern_counts = hist.ctypes.data_as(ctypes.POINTER(ctypes.c_uint64))
+    red = None
+    if reduce and shard[1] > 1:
+        from . import parallel
+        red = parallel.reduce_buffer(hist.size if hist is not None else 0, shard[1])
+        if red is not None:
+            cfg.reduce_out = red.data_ptr()
     t0 = time.perf_counter()
     _native.check(_native.load().wm_run(h, ctypes.byref(a), ctypes.byref(cfg), ctypes.byref(res)))
     wall = time.perf_counter() - t0
@@ -312,7 +335,10 @@ def run(g: CsrGraph, app: Application, *, mode: str = "wc", warps: int = None,
         extra={"bucket_words": res.bucket_words, "nodes": int(res.nodes),
                "polls": int(res.polls), "build_ms": res.build_ms,
                "h2d_bytes": int(res.h2d_bytes), "d2h_bytes": int(res.d2h_bytes)})
-    if reduce and shard[1] > 1:
+    if red is not None:
+        from . import parallel
+        out = parallel.allreduce_device(out, red, stream)
+    elif reduce and shard[1] > 1:
         from . import parallel
         out = parallel.allreduce_result(out)
     return out

@@ -5,14 +5,20 @@ The path shards naturally: root subtrees are independent
 (``engine.py:821-826``, ``aggregate.py:39-55``).  One process per GPU;
 rank ``r`` of ``N`` takes the cost-sorted root tasks ``i ≡ r (mod N)``
 (computed identically on every rank inside ``wm_run``), runs its own
-on-device load balancer, and the ranks combine
-``[clique_count, leaves, alg_bytes, hist[P]]`` with ONE
-``all_reduce(SUM)`` over NCCL (gloo on CPU for the host-logic tests).
+on-device load balancer, and the ranks combine their results with ONE
+``all_reduce(SUM)``: ``wm_run`` writes ``[cliques, leaves, B_alg,
+migrations, donations, tasks, records, checksum, hist[P], timing slots]``
+into a device buffer on the run's stream (``wm_cfg.reduce_out``) and the
+collective runs over that buffer on the same stream (NCCL), so nothing is
+copied to the host or repacked before the reduction.  gloo (CPU tests, and
+several ranks sharing one GPU) reduces a host copy of the same vector.
 """
 
 from __future__ import annotations
 
 from dataclasses import replace
+
+import numpy as np
 
 
 def _dist():
@@ -82,3 +88,70 @@ def allreduce_result(res, group=None, device=None):
                    kernel_ms=tt[0], device_ms=tt[1], wall_seconds=tt[2],
                    idle_warp_fraction=tt[3], idle_warp_fraction_tail=tt[4],
                    devices=dist.get_world_size(group))
+
+
+def reduce_buffer(pattern_count: int, world: int):
+    """Device buffer for ``wm_cfg.reduce_out`` (``wm_reduce_words`` int64
+    words on the current device), or None without a process group."""
+    if _dist() is None:
+        return None
+    import torch
+    from . import _native
+    words = int(_native.load().wm_reduce_words(pattern_count, world))
+    return torch.empty(words, dtype=torch.int64,
+                       device=torch.device("cuda", torch.cuda.current_device()))
+
+
+def _torch_stream(stream):
+    import torch
+    if stream is None:
+        return torch.cuda.current_stream()
+    if isinstance(stream, int):
+        return torch.cuda.ExternalStream(stream)
+    return stream
+
+
+def allreduce_device(res, vec, stream=None, group=None):
+    """ONE all_reduce(SUM) over the device result vector ``wm_run`` wrote
+    on ``stream`` (layout: include/warpmine_b200.h ``WM_RED_*``), then one
+    copy of the reduced vector to the host.  Counters are sums mod 2^64;
+    each rank's timing slot survives the sum, so ``kernel_ms`` etc. are the
+    max over ranks (the job's critical path)."""
+    import torch
+    from . import _native
+    dist = _dist()
+    if dist is None:
+        return res
+    world = dist.get_world_size(group)
+    if dist.get_backend(group) == "nccl":
+        with torch.cuda.stream(_torch_stream(stream)):
+            dist.all_reduce(vec, op=dist.ReduceOp.SUM, group=group)
+            host = vec.cpu()
+    else:  # gloo reduces host tensors
+        if vec.is_cuda:
+            with torch.cuda.stream(_torch_stream(stream)):
+                host = vec.cpu()
+        else:
+            host = vec.clone()
+        dist.all_reduce(host, op=dist.ReduceOp.SUM, group=group)
+    v = host.numpy()
+    u = v.view(np.uint64)
+    P = len(res.pattern_counts) if res.pattern_counts is not None else 0
+    base = _native.WM_RED_HIST + P
+    slots = v[base:base + _native.WM_RED_SLOT_WORDS * world].view(np.float64)
+    tmax = slots.reshape(world, _native.WM_RED_SLOT_WORDS).max(axis=0)
+    return replace(res,
+                   clique_count=int(u[_native.WM_RED_CLIQUES])
+                   if res.clique_count is not None else None,
+                   aggregated_total=int(u[_native.WM_RED_LEAVES]),
+                   alg_bytes=int(u[_native.WM_RED_ALG_BYTES]),
+                   migrations=int(u[_native.WM_RED_MIGRATIONS]),
+                   rebalance_count=int(u[_native.WM_RED_DONATIONS]),
+                   tasks=int(u[_native.WM_RED_TASKS]),
+                   pattern_counts=[int(x) for x in u[_native.WM_RED_HIST:base]]
+                   if res.pattern_counts is not None else None,
+                   kernel_ms=float(tmax[0]), device_ms=float(tmax[1]),
+                   idle_warp_fraction=float(tmax[2]), idle_warp_fraction_tail=float(tmax[3]),
+                   devices=world,
+                   extra=dict(res.extra, collective="all_reduce(SUM) x1 over %d words (%s)"
+                              % (v.size, dist.get_backend(group))))

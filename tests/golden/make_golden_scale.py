@@ -87,7 +87,7 @@ def main():
     r4.update({"digest": digest(g4), "n": g4.n, "m": g4.m, "max_degree": g4.max_degree,
                "recipe": "rmat(20, 16, a=.57, b=.19, c=.19, seed=1), ids permuted (seed 20)"})
     suf = r4.setdefault("motif_suffix", {})
-    for k, s in ((5, 16384), (6, 4096), (5, 4096), (7, 2048)):
+    for k, s in ((5, 16384), (6, 4096), (5, 4096), (7, 2048), (6, 8192), (6, 16384)):
         key = "k%d_s%d" % (k, s)
         if key in suf:
             continue

@@ -37,8 +37,21 @@ def test_library_exports_every_declared_symbol():
     for name in header_functions():
         assert hasattr(lib, name), name
     L = _native.load()
-    assert L.wm_abi_version() == 1
+    assert L.wm_abi_version() == _native.ABI_VERSION == 2
     assert L.wm_last_error() == b""
+
+
+def test_reduce_vector_layout():
+    """wm_reduce_words and the WM_RED_* constants agree between header and
+    binding (host-only call, no device work)."""
+    from paper_2212_04551_b200 import _native
+    src = open(os.path.join(ROOT, "include", "warpmine_b200.h")).read()
+    consts = dict((k, int(v)) for k, v in re.findall(r"#define (WM_RED_\w+) (\d+)", src))
+    for k, v in consts.items():
+        assert getattr(_native, k) == v, k
+    L = _native.load()
+    assert L.wm_reduce_words(0, 1) == consts["WM_RED_HIST"] + consts["WM_RED_SLOT_WORDS"]
+    assert L.wm_reduce_words(853, 8) == consts["WM_RED_HIST"] + 853 + 8 * consts["WM_RED_SLOT_WORDS"]
 
 
 def test_struct_layouts_match_header():

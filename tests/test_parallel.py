@@ -79,3 +79,52 @@ def test_shards_partition_tasks():
     tasks = list(range(101))
     parts = [parallel.shard_tasks(tasks, r, 4) for r in range(4)]
     assert sorted(sum(parts, [])) == tasks
+
+
+def _vec_worker(rank, world, port, out):
+    """Each rank holds the device result vector wm_run would write (layout of
+    include/warpmine_b200.h WM_RED_*); allreduce_device sums it once."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2212_04551_b200 import _native, parallel
+    from paper_2212_04551_b200.engine import RunResult
+    P = 6
+    v = np.zeros(_native.WM_RED_HIST + P + _native.WM_RED_SLOT_WORDS * world, dtype=np.uint64)
+    v[_native.WM_RED_LEAVES] = 100 + rank
+    v[_native.WM_RED_ALG_BYTES] = (1 << 63) + rank      # sums wrap mod 2^64
+    v[_native.WM_RED_MIGRATIONS] = 3
+    v[_native.WM_RED_DONATIONS] = 2
+    v[_native.WM_RED_TASKS] = 10 * (rank + 1)
+    v[_native.WM_RED_HIST:_native.WM_RED_HIST + P] = np.arange(P) + rank
+    slot = _native.WM_RED_HIST + P + _native.WM_RED_SLOT_WORDS * rank
+    v[slot:slot + 4] = np.array([1.5 + rank, 2.0, 0.25 * (rank + 1), 0.5],
+                                dtype=np.float64).view(np.uint64)
+    res = RunResult(app="motifs", k=4, mode="opt", warps=1, lane_width=32,
+                    clique_count=None, pattern_counts=[0] * P, records_emitted=None,
+                    aggregated_total=0, ledgers=[], makespan_ticks=0, wall_seconds=0.0,
+                    rebalance_count=0, migrations=0, peak_extension_storage=0)
+    red = parallel.allreduce_device(res, torch.from_numpy(v.view(np.int64)))
+    out[rank] = (red.aggregated_total, red.alg_bytes, red.migrations, red.rebalance_count,
+                 red.tasks, red.pattern_counts, red.kernel_ms, red.device_ms,
+                 red.idle_warp_fraction, red.devices, red.clique_count,
+                 red.extra["collective"])
+    dist.destroy_process_group()
+
+
+def test_device_result_vector_single_allreduce():
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_vec_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    for rank in range(2):
+        leaves, ab, mig, don, tasks, hist, kms, dms, idle, dev, cc, coll = out[rank]
+        assert leaves == 201
+        assert ab == 1                     # (2^63 + 0) + (2^63 + 1) mod 2^64
+        assert (mig, don, tasks) == (6, 4, 30)
+        assert hist == [2 * i + 1 for i in range(6)]
+        assert (kms, dms, idle) == (2.5, 2.0, 0.5)   # max over ranks
+        assert dev == 2 and cc is None
+        assert coll.startswith("all_reduce(SUM) x1")
