@@ -98,7 +98,8 @@ typedef struct {
   int shard_count;          /*   (multi-GPU, one process per GPU); 1 = all */
   int order;                /* WM_ORDER_* (clique only) */
   int count_bytes;          /* 1: instrumented pass computing B_alg (SURVEY
-                               8(d)); forces LB off */
+                               8(d)); cliques run it with LB off, motifs
+                               with the balancer as configured */
   int warps_per_block;      /* 0 = auto */
   int blocks_per_sm;        /* 0 = auto (occupancy) */
   void *stream;             /* cudaStream_t to run on; NULL = library stream */

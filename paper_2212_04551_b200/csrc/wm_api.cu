@@ -176,7 +176,9 @@ int red_edges(const wm_cfg *cfg, cudaStream_t s, const int64_t *nnz) {
 // CsrGraph.validate (graph.py:122-133) on the device, warp per vertex.  The
 // first violation in the reference's check order wins: vertex u ascending,
 // then per u: range/offsets, strictly ascending, self-loop, symmetry (first v
-// in row order).  Key = u << 33 | code << 31 | detail; atomicMin.
+// in row order).  Key = u << 33 | code << 31 | detail; atomicMin.  Offsets
+// that decrease are reported first (the reference checks them before any row,
+// graph.py:124-125): their own word, bad[1] = min vertex.
 enum : unsigned long long { kCsrRange = 0, kCsrAscend = 1, kCsrLoop = 2, kCsrSym = 3 };
 
 __global__ void csr_check_kernel(int64_t n, int64_t nnz, const int64_t *__restrict__ off,
@@ -188,7 +190,7 @@ __global__ void csr_check_kernel(int64_t n, int64_t nnz, const int64_t *__restri
     int64_t b = off[u], e = off[u + 1];
     unsigned long long key = ~0ull;
     if (e < b || b < 0 || e > nnz) {
-      key = ((unsigned long long)u << 33) | (kCsrRange << 31);  // detail 0: offsets
+      if (lane == 0) atomicMin(bad + 1, (unsigned long long)u);
     } else {
       for (int64_t p0 = b; p0 < e; p0 += 32) {
         const int64_t p = p0 + lane;
@@ -234,22 +236,24 @@ __global__ void csr_check_kernel(int64_t n, int64_t nnz, const int64_t *__restri
 static int csr_validate(Graph *g, cudaStream_t s) {
   int st = g->ws->counters.ensure(sizeof(unsigned long long) * 64);
   if (st) return st;
-  unsigned long long *bad = g->ws->counters.as<unsigned long long>() + 63;
-  WM_CUDA(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), s));
+  unsigned long long *bad = g->ws->counters.as<unsigned long long>() + 62;
+  WM_CUDA(cudaMemsetAsync(bad, 0xff, 2 * sizeof(unsigned long long), s));
   const int64_t want = (g->n * 32 + 255) / 256;
   const int blocks = (int)(want < (int64_t)g->num_sms * 16 ? want : (int64_t)g->num_sms * 16);
   csr_check_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(g->n, g->nnz, g->offsets,
                                                            g->neighbors, bad);
   WM_CUDA(cudaGetLastError());
-  unsigned long long h = ~0ull;
-  WM_CUDA(cudaMemcpyAsync(&h, bad, sizeof h, cudaMemcpyDeviceToHost, s));
+  unsigned long long hb[2] = {~0ull, ~0ull};
+  WM_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
+  if (hb[1] != ~0ull)
+    return fail(WM_EINVAL, "offsets must be non-decreasing (vertex %lld)", (long long)hb[1]);
+  const unsigned long long h = hb[0];
   if (h == ~0ull) return WM_OK;
   const long long u = (long long)(h >> 33);
   const unsigned long long code = (h >> 31) & 3ull, det = h & 0x7FFFFFFFull;
   switch (code) {
     case kCsrRange:
-      if (det == 0) return fail(WM_EINVAL, "offsets must be non-decreasing (vertex %lld)", u);
       return fail(WM_EINVAL, "neighbour #%llu of vertex %lld is outside [0, %lld)", det - 1, u,
                   (long long)g->n);
     case kCsrAscend:

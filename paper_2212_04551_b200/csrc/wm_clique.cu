@@ -778,7 +778,16 @@ __device__ __forceinline__ unsigned long long bulk5_round(const uint32_t *R, uin
     const uint32_t cij = c & R[h] & R[i] & R[j];
     uint32_t m = cij;
     m &= m - 1u;  // rows are lower-triangular: the lowest member adds nothing
+#if WM_BULK5_ILP2
+    // two members per trip: independent LDS/POPC chains, half the branches
+    while (m) {
+      const uint32_t r1 = R[pop_hi(m)];
+      const uint32_t r2 = m ? R[pop_hi(m)] : 0u;
+      part += __popc(cij & r1) + __popc(cij & r2);
+    }
+#else
     while (m) part += __popc(cij & R[pop_hi(m)]);
+#endif
   }
   return part;
 }

@@ -380,6 +380,7 @@ struct Workspace {
   DeviceBuffer dag_off, dag_nbr, outdeg, keys_in, keys_out, vals_in, vals_out, cub_tmp;
   DeviceBuffer lb, ring, counters, hist, arena, table, listing, listing_ring;
   DeviceBuffer edge_src, edge_flag, edge_pos;  // clique orientation, per directed edge
+  DeviceBuffer claims;  // motif B_alg claim slots (count_bytes with the balancer on)
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 

@@ -107,6 +107,10 @@ struct MotifArgs {
   unsigned long long *counters;    // [0] leaves [1] B_alg [2] tasks [3] nodes [4] polls [5] peak
   int lb_on, lb_poll, idle_min;
   int smem_hist;
+  // B_alg claim slots (BYTES): one u32 flag per shared (donated-across) node
+  uint32_t *claims;
+  unsigned long long *claim_ctr;
+  uint32_t claim_cap;
   EdgeHash H;                      // adjacency probes (null table: CSR binary search)
   LbShared L;
   ListRing ring;
@@ -120,8 +124,15 @@ struct MotifWarp {
   int32_t le[32];                   // listing: leaf vertex of record rank r
   uint32_t lm[32];                  //          and its adjacency mask
   uint32_t size[kMaxK], cur[kMaxK], lo[kMaxK];
-  unsigned long long below[kMaxK];  // leaves under the node of length L
+  // B_alg: the node of length L is productive iff a leaf lies
+  // below it.  claimed bit L: this warp knows the node's bytes are counted
+  // (by itself or another warp); claim[L]: global claim slot of a node shared
+  // with other warps through a donation (kNoClaim: private to this warp).
+  uint32_t claim[kMaxK];
+  uint32_t claimed;
 };
+
+constexpr uint32_t kNoClaim = 0xFFFFFFFFu;
 
 __device__ __forceinline__ int group_off(int i) { return i * (i - 1) / 2 - 1; }
 
@@ -508,6 +519,47 @@ __device__ __forceinline__ void set_tr(const MotifArgs &a, MotifWarp &w, int j, 
 }
 
 constexpr int kMotifHdr = 6;  // [root, level, lo, hi, bitmap lo, bitmap hi] then tr[1..level)
+// BYTES records also carry the donor's claimed mask and claim slots of the
+// shared nodes 1..level: word kMotifClaimMask, then kMotifClaim + L - 1
+constexpr int kMotifClaimMask = kMotifHdr + kMaxK - 1;
+constexpr int kMotifClaim = kMotifHdr + kMaxK;
+constexpr int kMotifRecWords = kMotifClaim + kMaxK;
+
+// A leaf-parent node of length L produced leaves: it and every ancestor are
+// productive.  Count each node's 4 * deg(last) exactly once over all warps:
+// private nodes directly, shared nodes through their claim slot (first
+// atomicExch wins).  A claimed node's ancestors are claimed already, so the
+// walk stops at the first one.  Lane 0.
+__device__ __forceinline__ void claim_path(const MotifArgs &a, MotifWarp &w, int L,
+                                           unsigned long long &bytes) {
+  for (; L >= 1; --L) {
+    if ((w.claimed >> L) & 1u) break;
+    w.claimed |= 1u << L;
+    const uint32_t c = w.claim[L];
+    if (c == kNoClaim || atomicExch(a.claims + c, 1u) == 0u) {
+      bytes += 4ull * (unsigned long long)(w.te[L - 1] - w.tb[L - 1]);
+    } else {
+      w.claimed |= (1u << L) - 1u;  // another warp claimed this node and its ancestors
+      break;
+    }
+  }
+}
+
+// Before donating children of the node of length sd: give every unclaimed
+// private node 1..sd a global claim slot (the thief shares them).  Lane 0;
+// false when the slot table is full (the caller then skips the donation).
+__device__ __forceinline__ bool share_claims(const MotifArgs &a, MotifWarp &w, int sd) {
+  int need = 0;
+  for (int L = 1; L <= sd; ++L)
+    if (!((w.claimed >> L) & 1u) && w.claim[L] == kNoClaim) ++need;
+  if (!need) return true;
+  const unsigned long long base = atomicAdd(a.claim_ctr, (unsigned long long)need);
+  if (base + need > a.claim_cap) return false;
+  uint32_t c = (uint32_t)base;
+  for (int L = 1; L <= sd; ++L)
+    if (!((w.claimed >> L) & 1u) && w.claim[L] == kNoClaim) w.claim[L] = c++;
+  return true;
+}
 
 // a leaf-level range is donated only if it carries >= this many candidate scans
 #ifndef WM_MOTIF_DONATE_MIN
@@ -556,7 +608,8 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
       set_tr(a, w, 0, __ldg(a.tasks + a.task_offset + ti * a.task_stride));
       if (lane == 0) {
         w.bm[0] = 0;
-        w.below[1] = 0;
+        w.claimed = 0;
+        w.claim[1] = kNoClaim;
       }
       __syncwarp();
       const uint32_t n1 = build_first(a, w, base);
@@ -583,11 +636,20 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
         if (lane == 0) w.size[j + 1] = n;
         __syncwarp();
       }
+      if (BYTES) {
+        const uint32_t cm = rec_word(rec, kMotifClaimMask);
+        uint32_t cl[kMaxK];
+#pragma unroll
+        for (int j = 1; j < kMaxK; ++j) cl[j] = rec_word(rec, kMotifClaim + j - 1);
+        if (lane == 0) {
+          w.claimed = cm;
+          for (int j = 1; j <= s0; ++j) w.claim[j] = cl[j];
+        }
+      }
       if (lane == 0) {
         w.bm[s0 - 1] = bm;
         w.cur[s0] = hi;
         w.lo[s0] = lo;
-        w.below[s0] = 0;
       }
 #if WM_MOTIF_PROF
       prof[6] += 1;
@@ -600,14 +662,6 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
       const uint32_t cur = w.cur[s];
       if (cur == w.lo[s]) {
         // level exhausted: the node of length s is complete
-        if (BYTES && lane == 0) {
-          const unsigned long long b = w.below[s];
-          if (b) {
-            bytes += 4ull * (unsigned long long)(w.te[s - 1] - w.tb[s - 1]);
-            if (s > s0) w.below[s - 1] += b;
-          }
-        }
-        __syncwarp();
         if (s == s0) break;
         --s;
         continue;
@@ -625,6 +679,10 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
       const uint32_t m = ent >> a.vbits;
       set_tr(a, w, s, v);
       if (lane == 0) {
+        if (BYTES) {  // a fresh node of length s + 1
+          w.claimed &= ~(1u << (s + 1));
+          w.claim[s + 1] = kNoClaim;
+        }
         w.cur[s] = cur - 1;
         // induce (engine.py:678-705): bitmap of tr[0..s] (s+1 vertices)
         w.bm[s] = (s == 1) ? 0ull
@@ -650,10 +708,7 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
         }
 #endif
         leaves += got;
-        if (BYTES && lane == 0 && got) {
-          bytes += 4ull * (unsigned long long)(w.te[s] - w.tb[s]);
-          w.below[s] += got;
-        }
+        if (BYTES && lane == 0 && got) claim_path(a, w, s + 1, bytes);
         __syncwarp();
       } else {
         WM_PT(tb);
@@ -665,7 +720,6 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
           w.size[s + 1] = n;
           w.cur[s + 1] = n;
           w.lo[s + 1] = 0;
-          w.below[s + 1] = 0;
         }
         __syncwarp();
         unsigned long long live = 0;
@@ -674,7 +728,7 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
         ++s;
       }
       // on-device load balancing: donate half of the shallowest pending range
-      if (!BYTES && a.lb_on && ++poll >= a.lb_poll) {
+      if (a.lb_on && ++poll >= a.lb_poll) {
         poll = 0;
         ++polls;
         if (donation_wanted(a.L, a.idle_min)) {
@@ -683,8 +737,13 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
             if (w.cur[j] - w.lo[j] >= 2u) { sd = j; break; }
           if (sd >= 0) {
             const uint32_t pend = w.cur[sd] - w.lo[sd];
-            const bool worth =
+            bool worth =
                 sd < k - 2 || (unsigned long long)pend * w.size[sd] >= WM_MOTIF_DONATE_MIN;
+            if (BYTES && worth) {
+              int ok_share = 0;
+              if (lane == 0) ok_share = share_claims(a, w, sd);
+              worth = __shfl_sync(0xffffffffu, ok_share, 0) != 0;
+            }
             if (worth) {
               const uint32_t half = pend / 2;
               const uint32_t lo = w.lo[sd];
@@ -700,6 +759,9 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
                 else if (idx == 4) val = (uint32_t)w.bm[sd - 1];
                 else if (idx == 5) val = (uint32_t)(w.bm[sd - 1] >> 32);
                 else if (idx >= kMotifHdr && idx < kMotifHdr + sd - 1) val = (uint32_t)w.tr[idx - kMotifHdr + 1];
+                else if (BYTES && idx == kMotifClaimMask) val = w.claimed & ((2u << sd) - 1u);
+                else if (BYTES && idx >= kMotifClaim && idx < kMotifClaim + sd)
+                  val = w.claim[idx - kMotifClaim + 1];
                 r.w[q] = val;
               }
               donate_record(a.L, r);
@@ -1025,7 +1087,9 @@ static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s
     return g->ws->ring.ensure(sizeof(uint32_t) * kSlotWords * (size_t)cap);
   }
   a.arena = g->ws->arena.as<uint32_t>();
-  if ((st = lb_prepare(g, a.L.lb, warps, (uint32_t)(kMotifHdr + kMaxK), &a.L, s))) return st;
+  if ((st = lb_prepare(g, a.L.lb, warps, (uint32_t)(BYTES ? kMotifRecWords : kMotifHdr + kMaxK),
+                      &a.L, s)))
+    return st;
   a.idle_min = (int)((1.0 - cfg->lb_threshold) * warps);
   if (a.idle_min < 1) a.idle_min = 1;
   WM_CUDA(cudaEventRecord(k0, s));  // after all host-side setup: kernel time only
@@ -1225,7 +1289,8 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   const int64_t n = g->n;
   const int k = app->k;
   const bool bytes = cfg->count_bytes != 0;
-  const bool lb_on = cfg->mode == WM_MODE_OPT && !bytes;
+  // B_alg works with the balancer on (claim slots, motif_enum_kernel<true>)
+  const bool lb_on = cfg->mode == WM_MODE_OPT;
   const int vbits = 32 - (k - 2);
   if (n > (1ll << vbits))
     return fail(WM_EINVAL, "motif kernel packs vertex ids in %d bits; n=%lld too large for k=%d",
@@ -1310,6 +1375,17 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   a.lb_poll = cfg->lb_poll > 0 ? cfg->lb_poll : 1;
   a.idle_min = 1;
   a.smem_hist = app->pattern_count <= 2048;
+  a.claims = nullptr;
+  a.claim_ctr = ctr + 16;
+  a.claim_cap = 0;
+  if (bytes) {
+    // claim slots for nodes shared through donations (untimed allocation)
+    const uint32_t cap = 1u << 24;
+    if ((st = g->ws->claims.ensure(sizeof(uint32_t) * cap))) return st;
+    WM_CUDA(cudaMemsetAsync(g->ws->claims.ptr, 0, sizeof(uint32_t) * cap, s));
+    a.claims = g->ws->claims.as<uint32_t>();
+    a.claim_cap = cap;
+  }
   a.H.b = nullptr;
   a.H.bmask = 0;
   // WM_NO_EDGE_HASH=1 forces the CSR binary-search probes (fallback-path tests)

@@ -42,6 +42,32 @@ def test_motif_alg_bytes_match_reference(golden, cuda):
         assert res.alg_bytes == r["alg_bytes"], (e["name"], r["k"], res.alg_bytes, r["alg_bytes"])
 
 
+def test_motif_alg_bytes_with_balancer(golden, scale_golden, cuda):
+    """B_alg with the on-device balancer forced on (threshold 1.0, poll 1):
+    productive nodes shared through donations are counted exactly once
+    (claim slots), so it equals the LB-off / reference figure."""
+    from paper_2212_04551_b200 import BalanceConfig, run_motifs, synth
+    lb = BalanceConfig(threshold=1.0, poll_interval=1)
+    n = 0
+    for g, e, r in _cases(golden):
+        res = run_motifs(g, r["k"], dictionary(r["k"]), mode="opt", balance_config=lb,
+                         count_bytes=True)
+        assert res.alg_bytes == r["alg_bytes"], (e["name"], r["k"], res.alg_bytes, r["alg_bytes"])
+        assert res.pattern_counts == r["hist"]
+        n += 1
+    assert n > 0
+    migr = 0
+    for name in ("cfg1", "cfg2"):
+        g = synth.config_graph(name)
+        for k, want in scale_golden[name]["motif"].items():
+            res = run_motifs(g, int(k), dictionary(int(k)), mode="opt", balance_config=lb,
+                             count_bytes=True)
+            assert res.alg_bytes == want["alg_bytes"], (name, k, res.alg_bytes)
+            assert res.pattern_counts == want["hist"]
+            migr += res.migrations
+    assert migr > 0  # donations happened
+
+
 def test_known_answers(cuda):
     """Reference tests/test_apps.py:57-72."""
     from paper_2212_04551_b200 import CsrGraph, complete_graph, motif_counting, path_graph

@@ -4,6 +4,8 @@ engine) against golden vectors produced by the reference itself
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import pytest
 
@@ -97,3 +99,26 @@ def test_scale_golden_pinned(scale_golden):
     assert [cl[str(k)]["count"] for k in range(3, 10)] == want
     assert scale_golden["cfg3"]["id_order_k3"]["count"] == want[0]
     assert scale_golden["cfg3"]["m"] == 947479
+
+
+def test_oracle_matches_reference_on_config_slices():
+    """The C restatement against the REFERENCE's own results on slices of
+    configs 3-5 (tests/golden/ref_scale_golden.json, make_golden_ref_scale.py)."""
+    import json
+    import numpy as np
+    from conftest import GOLDEN_DIR, dictionary
+    from paper_2212_04551_b200 import synth
+    with open(os.path.join(GOLDEN_DIR, "ref_scale_golden.json")) as fh:
+        ref = json.load(fh)
+    g3 = synth.config_graph("cfg3")
+    for key, want in ref["cfg3"]["clique_roots"].items():
+        b, e = want["roots"]
+        got = oracle.clique_run(g3, want["k"], roots=np.arange(b, e))
+        assert got["count"] == want["count"], key
+    g4 = synth.config_graph("cfg4")
+    for key, want in ref["cfg4"]["motif_suffix"].items():
+        k, s = want["k"], want["suffix"]
+        d = dictionary(k)
+        got = oracle.motif_run(g4, k, d.table, d.pattern_count, root_begin=g4.n - s,
+                               root_end=g4.n)
+        assert got["hist"] == want["hist"], key
