@@ -902,7 +902,11 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
 
 // Process one task (root or donated level) of word width w.
 template <int w, int WMAX, bool BYTES>
-#ifdef WM_RUNTASK_INLINE
+// inlined into the kernel (its three width instantiations): the out-of-line
+// form's call ABI kept a 272-byte local stack frame per thread (20.7 MB of
+// DRAM writes per launch) and cost cfg3 k=8 6.45 -> 5.77 ms, k=9 28.9 -> 26.6
+// (B200 A/B, profiles/r02_ab_clique1.log)
+#ifndef WM_RUNTASK_NOINLINE
 __device__ __forceinline__
 #else
 __device__ __noinline__
@@ -1322,33 +1326,6 @@ static int launch_enum(Graph *g, const wm_cfg *cfg, CliqueArgs a, const EnumPlan
 }
 
 // WM_PHASES=1: print per-phase device times of run_clique to stderr (tuning aid)
-struct PhaseTimer {
-  bool on = false;
-  cudaEvent_t ev[8];
-  const char *name[8];
-  int n = 0;
-  cudaStream_t s;
-  explicit PhaseTimer(cudaStream_t st) : s(st) {
-    const char *e = getenv("WM_PHASES");
-    on = e && *e == '1';
-  }
-  void mark(const char *nm) {
-    if (!on || n >= 8) return;
-    cudaEventCreate(&ev[n]);
-    cudaEventRecord(ev[n], s);
-    name[n++] = nm;
-  }
-  ~PhaseTimer() {
-    if (!on || n < 2) return;
-    cudaEventSynchronize(ev[n - 1]);
-    for (int i = 1; i < n; ++i) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
-      fprintf(stderr, "[wm phases] %-14s %8.3f ms\n", name[i], ms);
-    }
-    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
-  }
-};
 
 // --------------------------------------------------------------------------
 // Roots wider than the W=32 class (> 1024 out-neighbours): the k-cliques whose

@@ -24,6 +24,7 @@
 #include <atomic>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -382,6 +383,36 @@ struct Workspace {
   DeviceBuffer edge_src, edge_flag, edge_pos;  // clique orientation, per directed edge
   DeviceBuffer claims;  // motif B_alg claim slots (count_bytes with the balancer on)
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+};
+
+// Stream-ordered phase timing of the host-side run setup (WM_PHASES=1 prints
+// the per-phase device time to stderr; off by default).
+struct PhaseTimer {
+  bool on = false;
+  cudaEvent_t ev[12];
+  const char *name[12];
+  int n = 0;
+  cudaStream_t s;
+  explicit PhaseTimer(cudaStream_t st) : s(st) {
+    const char *e = getenv("WM_PHASES");
+    on = e && *e == '1';
+  }
+  void mark(const char *nm) {
+    if (!on || n >= 12) return;
+    cudaEventCreate(&ev[n]);
+    cudaEventRecord(ev[n], s);
+    name[n++] = nm;
+  }
+  ~PhaseTimer() {
+    if (!on || n < 2) return;
+    cudaEventSynchronize(ev[n - 1]);
+    for (int i = 1; i < n; ++i) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      fprintf(stderr, "[wm phases] %-14s %8.3f ms\n", name[i], ms);
+    }
+    for (int i = 0; i < n; ++i) cudaEventDestroy(ev[i]);
+  }
 };
 
 // returns the workspace of the current device (created on first use)

@@ -1313,7 +1313,9 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   if ((st = g->ws->cub_tmp.ensure(tmp_sort))) return st;
 
   cudaEvent_t e0 = g->ws->ev[0], e1 = g->ws->ev[1], k0 = g->ws->ev[2], k1 = g->ws->ev[3];
+  PhaseTimer pt(s);
   WM_CUDA(cudaEventRecord(e0, s));
+  pt.mark("start");
   unsigned long long *ctr = g->ws->counters.as<unsigned long long>();
   WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
   if (!lst) {
@@ -1338,9 +1340,11 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
       g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
       g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0,
       task_key_bits(g), s));
+  pt.mark("task sort");
   unsigned long long ntask = 0;
   WM_CUDA(cudaMemcpyAsync(&ntask, ctr + 8, sizeof ntask, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
+  pt.mark("sync");
   res->launches = 2;
   MotifArgs a;
   a.off = g->offsets;
@@ -1438,9 +1442,11 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   bytes ? launch_motif<true, false>(g, cfg, a, s, &warps, GO, k0)                \
          : (lst ? launch_motif<false, true>(g, cfg, a, s, &warps, GO, k0)        \
                 : launch_motif<false, false>(g, cfg, a, s, &warps, GO, k0)))
+  pt.mark("hash/claims");
   if (a.ntasks) {
     if ((st = WM_LAUNCH(false))) return st;
   }
+  pt.mark("plan");
   WM_CUDA(cudaEventRecord(k0, s));
   if (a.ntasks) {
     if ((st = WM_LAUNCH(true))) return st;
@@ -1448,6 +1454,7 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   }
 #undef WM_LAUNCH
   WM_CUDA(cudaEventRecord(k1, s));
+  pt.mark("lb init+kernel");
   int drain_st = WM_OK;
   if (lst) {
     // consume while the kernel produces (the host copies below would block)
@@ -1471,6 +1478,7 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   LbState hl;
   WM_CUDA(cudaMemcpyAsync(&hl, a.L.lb, sizeof hl, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaEventRecord(e1, s));
+  pt.mark("readback");
   WM_CUDA(cudaStreamSynchronize(s));
   float kms = 0, dms = 0;
   WM_CUDA(cudaEventElapsedTime(&kms, k0, k1));
