@@ -455,6 +455,7 @@ void wm_graph_destroy(void *gp) {
     if (g->neighbors) cudaFreeAsync(g->neighbors, s);
     if (g->ehash) cudaFreeAsync(g->ehash, s);
   }
+  clique_index_free(g);
   delete g;
 }
 

@@ -31,6 +31,7 @@
 // opt mode busy warps poll the idle-warp ring and donate half of their
 // shallowest pending extensions (balance.py:102-155 semantics: the thief owns
 // exactly the stolen branches; inherited levels are never regenerated).
+#include <algorithm>
 #include <cub/cub.cuh>
 #include <vector>
 
@@ -1473,6 +1474,155 @@ static int clique_wide_roots(Graph *g, const wm_app *app, const wm_cfg *cfg,
   return WM_OK;
 }
 
+
+// --------------------------------------------------------------------------
+// Per-(graph, orientation) clique index.  Everything the root tasks need that
+// depends only on the graph and the orientation — the oriented DAG (the
+// reference's filter_lower, engine.py:331-353, as a CSR), the cost-sorted
+// task order (all vertices by out-degree desc, id asc), the bitmap-arena
+// offsets of every task, and the member lists of the wide roots — is built
+// on the first clique run over all roots and kept on the graph handle, the
+// way the reference's CsrGraph keeps its adjacency lists/sets for every later
+// run (graph.py:93-103, used by engine.py:167-171).  A run over all roots
+// then plans on the host from the cached sorted out-degrees: the tasks of
+// k are the prefix with out-degree >= k-1, the width classes are sub-ranges
+// of it, and the run needs ONE host synchronisation (the result read-back).
+// Root-range runs, the DFS ablation and nested wide-root runs keep the
+// per-run path below.
+struct CliqueIndex {
+  int64_t *dag_off = nullptr;          // [n+1]
+  int32_t *dag_nbr = nullptr;          // [m]
+  int32_t *tasks = nullptr;            // [n] vertices by (out-degree desc, id asc)
+  unsigned long long *bm_off = nullptr;  // [n+1] arena offsets over `tasks` (wide: 0 words)
+  unsigned long long arena_words = 0;
+  std::vector<int32_t> sorted_deg;     // host: out-degree of tasks[i] (descending)
+  std::vector<std::vector<int32_t>> wide;  // host: members of the roots with d > 1024
+};
+
+void clique_index_free(Graph *g) {
+  for (int o = 0; o < 2; ++o) {
+    CliqueIndex *ix = static_cast<CliqueIndex *>(g->cidx[o]);
+    if (!ix) continue;
+    if (g->ws) {
+      cudaStream_t s = g->ws->own_stream;
+      cudaFreeAsync(ix->dag_off, s);
+      cudaFreeAsync(ix->dag_nbr, s);
+      cudaFreeAsync(ix->tasks, s);
+      cudaFreeAsync(ix->bm_off, s);
+    }
+    delete ix;
+    g->cidx[o] = nullptr;
+  }
+}
+
+__global__ void index_words_kernel(int64_t n, const uint32_t *__restrict__ keys,
+                                   unsigned long long *__restrict__ words) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t <= n;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int d = t < n ? (int)keys[t] - 1 : 0;
+    words[t] = d > 1024 ? 0ull : bm_words(d);  // wide roots live outside the arena
+  }
+}
+
+static int clique_index_get(Graph *g, int order, cudaStream_t s, CliqueIndex **out) {
+  const int o = order == WM_ORDER_ID ? 0 : 1;
+  if (g->cidx[o]) {
+    *out = static_cast<CliqueIndex *>(g->cidx[o]);
+    return WM_OK;
+  }
+  const int64_t n = g->n, nnz = g->nnz;
+  int st;
+  if ((st = g->ws->keys_in.ensure(sizeof(uint32_t) * n))) return st;
+  if ((st = g->ws->keys_out.ensure(sizeof(uint32_t) * n))) return st;
+  if ((st = g->ws->vals_in.ensure(sizeof(int32_t) * n))) return st;
+  if ((st = g->ws->outdeg.ensure(sizeof(int32_t) * (n + 1)))) return st;
+  if ((st = g->ws->hist.ensure(sizeof(unsigned long long) * (n + 1)))) return st;
+  if ((st = g->ws->edge_src.ensure(sizeof(int32_t) * (nnz + 1)))) return st;
+  if ((st = g->ws->edge_flag.ensure(sizeof(int32_t) * (nnz + 1)))) return st;
+  if ((st = g->ws->edge_pos.ensure(sizeof(int32_t) * (nnz + 1)))) return st;
+  size_t t1 = 0, t2 = 0, t3 = 0;
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t1, g->ws->edge_flag.as<int32_t>(),
+                                        g->ws->edge_pos.as<int32_t>(), (int)(nnz + 1), s));
+  WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+      nullptr, t2, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
+      g->ws->vals_in.as<int32_t>(), g->ws->vals_in.as<int32_t>(), (int)n, 0, 32, s));
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, g->ws->hist.as<unsigned long long>(),
+                                        g->ws->hist.as<unsigned long long>(), (int)(n + 1), s));
+  size_t tmp = t1 > t2 ? t1 : t2;
+  if (t3 > tmp) tmp = t3;
+  if ((st = g->ws->cub_tmp.ensure(tmp))) return st;
+  CliqueIndex *ix = new CliqueIndex();
+  auto alloc = [&](void **p, size_t b) {
+    return cudaMallocFromPoolAsync(p, b > 0 ? b : 4, g->ws->pool, s);
+  };
+  cudaError_t e = alloc(reinterpret_cast<void **>(&ix->dag_off), sizeof(int64_t) * (n + 1));
+  if (e == cudaSuccess)
+    e = alloc(reinterpret_cast<void **>(&ix->dag_nbr), sizeof(int32_t) * (nnz / 2 + 1));
+  if (e == cudaSuccess) e = alloc(reinterpret_cast<void **>(&ix->tasks), sizeof(int32_t) * n);
+  if (e == cudaSuccess)
+    e = alloc(reinterpret_cast<void **>(&ix->bm_off), sizeof(unsigned long long) * (n + 1));
+  if (e != cudaSuccess) {
+    g->cidx[o] = ix;
+    clique_index_free(g);
+    return fail(WM_ECUDA, "clique index allocation failed: %s", cudaGetErrorString(e));
+  }
+  g->cidx[o] = ix;  // owned by the graph from here on (freed with it)
+  const int tpb = 256;
+  const int64_t ns = (int64_t)g->num_sms;
+  const int vblocks = (int)((n * 32 + tpb - 1) / tpb < ns * 64 ? (n * 32 + tpb - 1) / tpb : ns * 64);
+  const int pblocks = (int)((nnz + tpb) / tpb < ns * 32 ? (nnz + tpb) / tpb : ns * 32);
+  const int nblocks = (int)((n + tpb) / tpb < ns * 16 ? (n + tpb) / tpb : ns * 16);
+  int32_t *esrc = g->ws->edge_src.as<int32_t>(), *eflag = g->ws->edge_flag.as<int32_t>(),
+          *epos = g->ws->edge_pos.as<int32_t>();
+  orient_src_kernel<<<vblocks, tpb, 0, s>>>(n, g->offsets, esrc);
+  orient_flag_kernel<<<pblocks, tpb, 0, s>>>(nnz, g->offsets, g->neighbors, esrc, order, eflag);
+  size_t tb = g->ws->cub_tmp.bytes;
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, eflag, epos, (int)(nnz + 1), s));
+  orient_scatter_kernel<<<pblocks, tpb, 0, s>>>(nnz, g->neighbors, eflag, epos, ix->dag_nbr);
+  orient_off_kernel<<<nblocks, tpb, 0, s>>>(n, g->offsets, epos, ix->dag_off,
+                                            g->ws->outdeg.as<int32_t>());
+  // every vertex is a task candidate (k = 1 keys: out-degree + 1)
+  task_keys_kernel<<<nblocks, tpb, 0, s>>>(n, g->ws->outdeg.as<int32_t>(), 1, 0, n,
+                                           g->ws->keys_in.as<uint32_t>(),
+                                           g->ws->vals_in.as<int32_t>());
+  tb = g->ws->cub_tmp.bytes;
+  WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+      g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
+      g->ws->vals_in.as<int32_t>(), ix->tasks, (int)n, 0, task_key_bits(g), s));
+  unsigned long long *words = g->ws->hist.as<unsigned long long>();
+  index_words_kernel<<<nblocks, tpb, 0, s>>>(n, g->ws->keys_out.as<uint32_t>(), words);
+  tb = g->ws->cub_tmp.bytes;
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, words, ix->bm_off, (int)(n + 1), s));
+  std::vector<uint32_t> keys((size_t)n);
+  WM_CUDA(cudaMemcpyAsync(keys.data(), g->ws->keys_out.ptr, sizeof(uint32_t) * n,
+                          cudaMemcpyDeviceToHost, s));
+  WM_CUDA(cudaMemcpyAsync(&ix->arena_words, ix->bm_off + n, sizeof ix->arena_words,
+                          cudaMemcpyDeviceToHost, s));
+  WM_CUDA(cudaStreamSynchronize(s));
+  ix->sorted_deg.resize((size_t)n);
+  for (int64_t i = 0; i < n; ++i) ix->sorted_deg[i] = (int32_t)keys[i] - 1;
+  // wide roots: the sorted prefix with d > 1024
+  int64_t nw = 0;
+  while (nw < n && ix->sorted_deg[nw] > 1024) ++nw;
+  if (nw) {
+    std::vector<int32_t> ids((size_t)nw);
+    std::vector<int64_t> off((size_t)n + 1);
+    WM_CUDA(cudaMemcpyAsync(ids.data(), ix->tasks, sizeof(int32_t) * nw, cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaMemcpyAsync(off.data(), ix->dag_off, sizeof(int64_t) * (n + 1),
+                            cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaStreamSynchronize(s));
+    for (int64_t i = 0; i < nw; ++i) {
+      std::vector<int32_t> M((size_t)(off[ids[i] + 1] - off[ids[i]]));
+      WM_CUDA(cudaMemcpyAsync(M.data(), ix->dag_nbr + off[ids[i]], sizeof(int32_t) * M.size(),
+                              cudaMemcpyDeviceToHost, s));
+      ix->wide.push_back(std::move(M));
+    }
+    WM_CUDA(cudaStreamSynchronize(s));
+  }
+  *out = ix;
+  return WM_OK;
+}
+
 int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s) {
   std::vector<std::vector<int32_t>> wide;
   int st = run_clique_impl(g, app, cfg, res, s, &wide, true);
@@ -1491,6 +1641,64 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   const bool bytes = cfg->count_bytes != 0;
   const bool lb_on = cfg->mode == WM_MODE_OPT && !bytes;
   int st;
+  // all roots, warp-centric, a user graph: plan from the cached index
+  const bool all_roots = (cfg->root_begin <= 0) &&
+                         (cfg->root_end < 0 || cfg->root_end >= n);
+  CliqueIndex *ix = nullptr;
+  if (top && all_roots && cfg->mode != WM_MODE_DFS) {
+    if ((st = clique_index_get(g, order, s, &ix))) return st;
+  }
+  if ((st = g->ws->counters.ensure(sizeof(unsigned long long) * 64))) return st;
+  if ((st = g->ws->lb.ensure(sizeof(LbState) * 8))) return st;
+  cudaEvent_t e0 = g->ws->ev[0], e1 = g->ws->ev[1], k0 = g->ws->ev[2], k1 = g->ws->ev[3], kb = g->ws->ev[4];
+  unsigned long long *ctr = g->ws->counters.as<unsigned long long>();
+  const int tpb = 256;
+  const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
+                                ? (n + tpb - 1) / tpb
+                                : (int64_t)g->num_sms * 16);
+  unsigned long long hb[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  unsigned long long skip = 0, ntask = 0, arena_words = 0;
+  const int64_t *doff_p = nullptr;
+  const int32_t *dnbr_p = nullptr;
+  int32_t *tasks_sorted = nullptr;
+  const unsigned long long *bm_off = nullptr;
+  if (ix) {
+    WM_CUDA(cudaEventRecord(e0, s));
+    pt.mark("start");
+    WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
+    // eligible tasks: the sorted prefix with out-degree >= k-1; buckets by
+    // width (d <= 32 << c), wide roots (d > 1024) first
+    const std::vector<int32_t> &sd = ix->sorted_deg;
+    auto count_ge = [&](int64_t x) {  // entries with degree >= x (descending order)
+      return (unsigned long long)(std::upper_bound(sd.begin(), sd.end(), (int32_t)x,
+                                                   [](int32_t v, int32_t e) { return v > e; }) -
+                                  sd.begin());
+    };
+    const unsigned long long E = count_ge(k - 1);
+    unsigned long long above = count_ge(1025);
+    if (above > E) above = E;
+    hb[6] = above;
+    for (int c = 5; c >= 0; --c) {
+      // bucket c: 32 << (c-1) < d <= 32 << c (bucket 0: d <= 32)
+      const unsigned long long lo_excl = c > 0 ? count_ge((32ll << (c - 1)) + 1) : E;
+      unsigned long long hi_incl = count_ge((32ll << c) + 1);
+      unsigned long long lo = lo_excl < E ? lo_excl : E;
+      if (hi_incl > E) hi_incl = E;
+      hb[c] = lo > hi_incl ? lo - hi_incl : 0;
+    }
+    skip = hb[6];
+    for (unsigned long long i = (unsigned long long)cfg->shard_rank; i < skip;
+         i += (unsigned long long)cfg->shard_count)
+      wide->push_back(ix->wide[i]);
+    for (int c = 0; c < 6; ++c) ntask += hb[c];
+    doff_p = ix->dag_off;
+    dnbr_p = ix->dag_nbr;
+    tasks_sorted = ix->tasks + skip;
+    bm_off = ix->bm_off + skip;
+    arena_words = ix->arena_words;
+    res->launches = 1;
+    pt.mark("plan");
+  } else {
   if ((st = g->ws->dag_off.ensure(sizeof(int64_t) * (n + 1)))) return st;
   if ((st = g->ws->outdeg.ensure(sizeof(int32_t) * (n + 1)))) return st;
   if ((st = g->ws->dag_nbr.ensure(sizeof(int32_t) * (g->nnz / 2 + 1)))) return st;
@@ -1500,8 +1708,6 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   if ((st = g->ws->vals_out.ensure(sizeof(int32_t) * n))) return st;
   if ((st = g->ws->hist.ensure(sizeof(unsigned long long) * (n + 1)))) return st;  // task words
   if ((st = g->ws->table.ensure(sizeof(unsigned long long) * (n + 1)))) return st; // bm_off
-  if ((st = g->ws->counters.ensure(sizeof(unsigned long long) * 64))) return st;
-  if ((st = g->ws->lb.ensure(sizeof(LbState) * 8))) return st;
   const int64_t nnz = g->nnz;
   if ((st = g->ws->edge_src.ensure(sizeof(int32_t) * (nnz + 1)))) return st;
   if ((st = g->ws->edge_flag.ensure(sizeof(int32_t) * (nnz + 1)))) return st;
@@ -1521,12 +1727,9 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   if (tmp_scan3 > tmp) tmp = tmp_scan3;
   if ((st = g->ws->cub_tmp.ensure(tmp))) return st;
 
-  cudaEvent_t e0 = g->ws->ev[0], e1 = g->ws->ev[1], k0 = g->ws->ev[2], k1 = g->ws->ev[3], kb = g->ws->ev[4];
   WM_CUDA(cudaEventRecord(e0, s));
   pt.mark("start");
-  unsigned long long *ctr = g->ws->counters.as<unsigned long long>();
   WM_CUDA(cudaMemsetAsync(ctr, 0, sizeof(unsigned long long) * 64, s));
-  const int tpb = 256;
   const int vblocks = (int)((n * 32 + tpb - 1) / tpb < (int64_t)g->num_sms * 64
                                 ? (n * 32 + tpb - 1) / tpb
                                 : (int64_t)g->num_sms * 64);
@@ -1548,9 +1751,6 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   pt.mark("orient");
   const int64_t rb = cfg->root_begin < 0 ? 0 : cfg->root_begin;
   const int64_t re = (cfg->root_end < 0 || cfg->root_end > n) ? n : cfg->root_end;
-  const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
-                                ? (n + tpb - 1) / tpb
-                                : (int64_t)g->num_sms * 16);
   task_keys_kernel<<<eblocks, tpb, 0, s>>>(n, g->ws->outdeg.as<int32_t>(), k, rb, re,
                                            g->ws->keys_in.as<uint32_t>(), g->ws->vals_in.as<int32_t>());
   tb = g->ws->cub_tmp.bytes;
@@ -1560,7 +1760,6 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
       task_key_bits(g), s));
   bucket_count_kernel<<<eblocks, tpb, 0, s>>>(n, g->ws->keys_out.as<uint32_t>(), ctr + 8);
   pt.mark("task sort");
-  unsigned long long hb[8];
   WM_CUDA(cudaMemcpyAsync(hb, ctr + 8, sizeof hb, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
   res->launches = 5;
@@ -1594,7 +1793,7 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   }
   // wide roots (> 1024 out-neighbours) sort first: hand this shard's share
   // (cyclic over their own list) to clique_wide_roots, skip them below
-  const unsigned long long skip = hb[6];
+  skip = hb[6];
   if (skip) {
     std::vector<int32_t> ids(skip);
     WM_CUDA(cudaMemcpyAsync(ids.data(), g->ws->vals_out.ptr, sizeof(int32_t) * skip,
@@ -1616,23 +1815,25 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
     res->d2h_bytes += sizeof(int32_t) * skip;
   }
   uint32_t *keys_sorted = g->ws->keys_out.as<uint32_t>() + skip;
-  int32_t *tasks_sorted = g->ws->vals_out.as<int32_t>() + skip;
-  unsigned long long ntask = 0;
+  tasks_sorted = g->ws->vals_out.as<int32_t>() + skip;
   for (int c = 0; c < 6; ++c) ntask += hb[c];
   // bitmap arena offsets: exclusive scan of d * ceil(d/32) over the sorted tasks
   unsigned long long *words = g->ws->hist.as<unsigned long long>();
-  unsigned long long *bm_off = g->ws->table.as<unsigned long long>();
-  unsigned long long arena_words = 0;
+  unsigned long long *bmo = g->ws->table.as<unsigned long long>();
   if (ntask) {
     task_words_kernel<<<eblocks, tpb, 0, s>>>(ntask, keys_sorted, words);
     WM_CUDA(cudaMemsetAsync(words + ntask, 0, sizeof(unsigned long long), s));
     tb = g->ws->cub_tmp.bytes;
-    WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, words, bm_off, (int)(ntask + 1), s));
-    WM_CUDA(cudaMemcpyAsync(&arena_words, bm_off + ntask, sizeof arena_words,
+    WM_CUDA(cub::DeviceScan::ExclusiveSum(g->ws->cub_tmp.ptr, tb, words, bmo, (int)(ntask + 1), s));
+    WM_CUDA(cudaMemcpyAsync(&arena_words, bmo + ntask, sizeof arena_words,
                             cudaMemcpyDeviceToHost, s));
     WM_CUDA(cudaStreamSynchronize(s));
     res->launches += 1;
   }
+  bm_off = bmo;
+  doff_p = g->ws->dag_off.as<int64_t>();
+  dnbr_p = g->ws->dag_nbr.as<int32_t>();
+  }  // per-run path
   if ((st = g->ws->arena.ensure(sizeof(uint32_t) * (arena_words + 1)))) return st;
 
   // width classes, contiguous in the descending sort: 32, 16, 8, then <= 4
@@ -1688,8 +1889,8 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
       const unsigned long long cnt = hb[c];
       if (!cnt) continue;
       CliqueArgs a;
-      a.doff = g->ws->dag_off.as<int64_t>();
-      a.dnbr = g->ws->dag_nbr.as<int32_t>();
+      a.doff = doff_p;
+      a.dnbr = dnbr_p;
       a.tasks = tasks_sorted + begin;
       a.bm_off = bm_off + begin;
       a.bm = g->ws->arena.as<uint32_t>();
@@ -1716,8 +1917,8 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
     }
     for (int i = 0; i < ncls && pass == 1; ++i) {
       CliqueArgs a;
-      a.doff = g->ws->dag_off.as<int64_t>();
-      a.dnbr = g->ws->dag_nbr.as<int32_t>();
+      a.doff = doff_p;
+      a.dnbr = dnbr_p;
       a.tasks = tasks_sorted + cls[i].begin;
       a.bm_off = bm_off + cls[i].begin;
       a.bm = g->ws->arena.as<uint32_t>();

@@ -462,7 +462,12 @@ struct Graph {
   // edge hash set (motif adjacency probes), built on first use; owned by the graph
   unsigned long long *ehash = nullptr;
   unsigned long long ehash_bmask = 0;  // bucket count - 1 (4 keys per bucket)
+  // clique index per orientation (id, degree), built on first use (wm_clique.cu)
+  void *cidx[2] = {nullptr, nullptr};
 };
+
+// frees g's clique indexes (wm_clique.cu)
+void clique_index_free(Graph *g);
 
 // Task sort keys are (out-)degree + 1 <= max_degree + 1: radix-sort only those
 // bits (same stable order as a 32-bit sort, fewer passes).
