@@ -32,6 +32,7 @@
 // rebuilds E_1..E_level for that prefix (same order, so the index range is
 // meaningful), exactly the reference's "inherited levels are generated but
 // empty" install (balance.py:131-155).
+#include <chrono>
 #include <cub/cub.cuh>
 
 #include "wm_common.cuh"
@@ -327,6 +328,25 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
   const uint32_t n_src = w.size[L];
   unsigned long long total = 0;
   bool bad = false;
+#if WM_MOTIF_UNROLL2
+  // two 32-entry chunks per trip: both chunks' entry loads, hash probes and
+  // dictionary lookups are independent, so they are in flight together
+  for (uint32_t i0 = 0; i0 < n_src; i0 += 64) {
+    const uint32_t ia = i0 + lane, ib = i0 + 32 + lane;
+    const uint32_t enta = ia < n_src ? __ldcg(src + ia) : 0u;
+    const uint32_t entb = ib < n_src ? __ldcg(src + ib) : 0u;
+    const int32_t ea = (int32_t)(enta & a.vmask), eb = (int32_t)(entb & a.vmask);
+    const bool va = ia < n_src && ea > x, vb = ib < n_src && eb > x;
+    const bool ha = va && adj_tr(a, w, L, ea);
+    const bool hb = vb && adj_tr(a, w, L, eb);
+    const uint32_t pa = va ? dict_lookup(a, bits | (((enta >> a.vbits) | ((uint32_t)ha << L)) << off)) : 0u;
+    const uint32_t pb = vb ? dict_lookup(a, bits | (((entb >> a.vbits) | ((uint32_t)hb << L)) << off)) : 0u;
+    bad |= (va && pa >= a.pattern_count) || (vb && pb >= a.pattern_count);
+    total += __popc(__ballot_sync(0xffffffffu, va)) + __popc(__ballot_sync(0xffffffffu, vb));
+    hist_add(a, sh, va && pa < a.pattern_count, pa);
+    if (i0 + 32 < n_src) hist_add(a, sh, vb && pb < a.pattern_count, pb);
+  }
+#else
   for (uint32_t i0 = 0; i0 < n_src; i0 += 32) {
     const uint32_t i = i0 + lane;
     bool valid = false;
@@ -344,6 +364,7 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     total += __popc(__ballot_sync(0xffffffffu, valid));
     hist_add(a, sh, valid && pid < a.pattern_count, pid);
   }
+#endif
   unsigned long long nb = 0;
   const long long pb = row_first_above(a.nbr, xb, xe, t0);
 #if WM_MOTIF_PROF
@@ -353,6 +374,16 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     atomicAdd(&a.counters[30], (unsigned long long)(xe - pb));
   }
 #endif
+#if WM_MOTIF_UNROLL2
+  for (long long p0 = pb; p0 < xe; p0 += 64) {
+    const long long p = p0 + lane, q = p0 + 32 + lane;
+    const int32_t e1 = p < xe ? __ldg(a.nbr + p) : -1;
+    const int32_t e2 = q < xe ? __ldg(a.nbr + q) : -1;
+    const bool k1 = e1 > t0 && adj_none(a, w, L, e1);
+    const bool k2 = e2 > t0 && adj_none(a, w, L, e2);
+    nb += __popc(__ballot_sync(0xffffffffu, k1)) + __popc(__ballot_sync(0xffffffffu, k2));
+  }
+#else
   for (long long p0 = pb; p0 < xe; p0 += 32) {
     const long long p = p0 + lane;
     bool keep = false;
@@ -362,6 +393,7 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     }
     nb += __popc(__ballot_sync(0xffffffffu, keep));
   }
+#endif
   if (nb) {
     const uint32_t pid = dict_lookup(a, bits | ((1u << L) << off));
     if (pid >= a.pattern_count) bad = true;
@@ -1068,12 +1100,16 @@ static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s
   if (cfg->blocks_per_sm > 0 && cfg->blocks_per_sm < bps) bps = cfg->blocks_per_sm;
   if (bps < 1) return fail(WM_ECAPACITY, "motif kernel does not fit on an SM");
   long long blocks = (long long)g->num_sms * bps;
-  // arena budget: per-warp levels 1..k-2 hold sum_L L*maxdeg entries
+  // arena budget: per-warp levels 1..k-2 hold sum_L L*maxdeg entries.  The
+  // free-memory query (a driver round trip) only when the grow-only arena
+  // does not already hold the full grid.
   const unsigned long long per_warp = a.warp_stride * sizeof(uint32_t);
-  size_t free_b = 0, total_b = 0;
-  WM_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const unsigned long long budget = (unsigned long long)(free_b * 0.6) + g->ws->arena.bytes;
-  while (blocks > 1 && (unsigned long long)blocks * wpb * per_warp > budget) blocks >>= 1;
+  if ((unsigned long long)blocks * wpb * per_warp > g->ws->arena.bytes) {
+    size_t free_b = 0, total_b = 0;
+    WM_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const unsigned long long budget = (unsigned long long)(free_b * 0.6) + g->ws->arena.bytes;
+    while (blocks > 1 && (unsigned long long)blocks * wpb * per_warp > budget) blocks >>= 1;
+  }
   if (!a.lb_on) {
     const unsigned long long need = (a.ntasks + wpb - 1) / wpb;
     if ((unsigned long long)blocks > need) blocks = (long long)(need > 0 ? need : 1);
@@ -1443,9 +1479,13 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
          : (lst ? launch_motif<false, true>(g, cfg, a, s, &warps, GO, k0)        \
                 : launch_motif<false, false>(g, cfg, a, s, &warps, GO, k0)))
   pt.mark("hash/claims");
+  const auto hp0 = std::chrono::steady_clock::now();
   if (a.ntasks) {
     if ((st = WM_LAUNCH(false))) return st;
   }
+  if (pt.on)
+    fprintf(stderr, "[wm phases] plan (host)     %8.3f ms\n",
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hp0).count());
   pt.mark("plan");
   WM_CUDA(cudaEventRecord(k0, s));
   if (a.ntasks) {
