@@ -741,6 +741,7 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
         }
         if (__shfl_sync(0xffffffffu, want, 0)) {
           // expose the pending children, donate, take back what is left
+          __syncwarp();  // every lane's read of Ps[q] precedes lane 0's write
           if (lane == 0) Ps[q] = pm;
           __syncwarp();
           try_donate<w>(sm.C, sm.P, a, s0, lv, task);
@@ -749,6 +750,7 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
         }
       }
     }
+    __syncwarp();  // (racecheck) reads of Ps[q] before the reset
     if (lane == 0) Ps[q] = 0u;
   }
   if (nq) {
@@ -779,16 +781,7 @@ __device__ __forceinline__ unsigned long long bulk5_round(const uint32_t *R, uin
     const uint32_t cij = c & R[h] & R[i] & R[j];
     uint32_t m = cij;
     m &= m - 1u;  // rows are lower-triangular: the lowest member adds nothing
-#if WM_BULK5_ILP2
-    // two members per trip: independent LDS/POPC chains, half the branches
-    while (m) {
-      const uint32_t r1 = R[pop_hi(m)];
-      const uint32_t r2 = m ? R[pop_hi(m)] : 0u;
-      part += __popc(cij & r1) + __popc(cij & r2);
-    }
-#else
     while (m) part += __popc(cij & R[pop_hi(m)]);
-#endif
   }
   return part;
 }

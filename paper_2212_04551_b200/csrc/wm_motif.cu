@@ -93,8 +93,12 @@ struct MotifArgs {
   // level-1 entries with index + root = l1_offset (mod l1_stride) (edge tasks
   // (r, u) dealt cyclically, rotated by the root so the many one-child roots
   // spread too); a hub root's subtree no longer lands on one
-  // GPU.  l1_stride = 1: no filter.
+  // GPU.  l1_stride = 1: no filter.  shard_level 2 (k >= 6) deals the
+  // level-2 entries (root, child, grandchild) instead, by a hash of the three
+  // vertex ids: one hub child's subtree no longer lands on one GPU either;
+  // every rank then builds E_2 of every child (a small share at k >= 6).
   uint32_t l1_offset, l1_stride;
+  int shard_level;
   int k;
   int vbits;
   uint32_t vmask;
@@ -328,25 +332,6 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
   const uint32_t n_src = w.size[L];
   unsigned long long total = 0;
   bool bad = false;
-#if WM_MOTIF_UNROLL2
-  // two 32-entry chunks per trip: both chunks' entry loads, hash probes and
-  // dictionary lookups are independent, so they are in flight together
-  for (uint32_t i0 = 0; i0 < n_src; i0 += 64) {
-    const uint32_t ia = i0 + lane, ib = i0 + 32 + lane;
-    const uint32_t enta = ia < n_src ? __ldcg(src + ia) : 0u;
-    const uint32_t entb = ib < n_src ? __ldcg(src + ib) : 0u;
-    const int32_t ea = (int32_t)(enta & a.vmask), eb = (int32_t)(entb & a.vmask);
-    const bool va = ia < n_src && ea > x, vb = ib < n_src && eb > x;
-    const bool ha = va && adj_tr(a, w, L, ea);
-    const bool hb = vb && adj_tr(a, w, L, eb);
-    const uint32_t pa = va ? dict_lookup(a, bits | (((enta >> a.vbits) | ((uint32_t)ha << L)) << off)) : 0u;
-    const uint32_t pb = vb ? dict_lookup(a, bits | (((entb >> a.vbits) | ((uint32_t)hb << L)) << off)) : 0u;
-    bad |= (va && pa >= a.pattern_count) || (vb && pb >= a.pattern_count);
-    total += __popc(__ballot_sync(0xffffffffu, va)) + __popc(__ballot_sync(0xffffffffu, vb));
-    hist_add(a, sh, va && pa < a.pattern_count, pa);
-    if (i0 + 32 < n_src) hist_add(a, sh, vb && pb < a.pattern_count, pb);
-  }
-#else
   for (uint32_t i0 = 0; i0 < n_src; i0 += 32) {
     const uint32_t i = i0 + lane;
     bool valid = false;
@@ -364,7 +349,6 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     total += __popc(__ballot_sync(0xffffffffu, valid));
     hist_add(a, sh, valid && pid < a.pattern_count, pid);
   }
-#endif
   unsigned long long nb = 0;
   const long long pb = row_first_above(a.nbr, xb, xe, t0);
 #if WM_MOTIF_PROF
@@ -374,16 +358,6 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     atomicAdd(&a.counters[30], (unsigned long long)(xe - pb));
   }
 #endif
-#if WM_MOTIF_UNROLL2
-  for (long long p0 = pb; p0 < xe; p0 += 64) {
-    const long long p = p0 + lane, q = p0 + 32 + lane;
-    const int32_t e1 = p < xe ? __ldg(a.nbr + p) : -1;
-    const int32_t e2 = q < xe ? __ldg(a.nbr + q) : -1;
-    const bool k1 = e1 > t0 && adj_none(a, w, L, e1);
-    const bool k2 = e2 > t0 && adj_none(a, w, L, e2);
-    nb += __popc(__ballot_sync(0xffffffffu, k1)) + __popc(__ballot_sync(0xffffffffu, k2));
-  }
-#else
   for (long long p0 = pb; p0 < xe; p0 += 32) {
     const long long p = p0 + lane;
     bool keep = false;
@@ -393,7 +367,6 @@ __device__ __forceinline__ unsigned long long aggregate_leaves(const MotifArgs &
     }
     nb += __popc(__ballot_sync(0xffffffffu, keep));
   }
-#endif
   if (nb) {
     const uint32_t pid = dict_lookup(a, bits | ((1u << L) << off));
     if (pid >= a.pattern_count) bad = true;
@@ -698,7 +671,7 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
         --s;
         continue;
       }
-      if (s == 1 && a.l1_stride > 1 &&
+      if (s == 1 && a.shard_level == 1 && a.l1_stride > 1 &&
           ((cur - 1) + (uint32_t)w.tr[0]) % a.l1_stride != a.l1_offset) {
         // another shard's edge task: consume without descending
         if (lane == 0) w.cur[1] = cur - 1;
@@ -708,6 +681,18 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
       // move_step: pop the highest pending entry (engine.py:652-669)
       const uint32_t ent = __ldcg(level_ptr(a, base, s) + (cur - 1));
       const int32_t v = (int32_t)(ent & a.vmask);
+      if (s == 2 && a.shard_level == 2 && a.l1_stride > 1) {
+        uint32_t h = (uint32_t)w.tr[0] * 0x9E3779B1u ^ (uint32_t)w.tr[1] * 0x85EBCA77u ^
+                     (uint32_t)v * 0xC2B2AE3Du;
+        h ^= h >> 15;
+        h *= 0x2C1B3C6Du;
+        h ^= h >> 12;
+        if (h % a.l1_stride != a.l1_offset) {  // another shard's (root, child, grandchild)
+          if (lane == 0) w.cur[2] = cur - 1;
+          __syncwarp();
+          continue;
+        }
+      }
       const uint32_t m = ent >> a.vbits;
       set_tr(a, w, s, v);
       if (lane == 0) {
@@ -775,6 +760,7 @@ __global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(Mot
               int ok_share = 0;
               if (lane == 0) ok_share = share_claims(a, w, sd);
               worth = __shfl_sync(0xffffffffu, ok_share, 0) != 0;
+              __syncwarp();  // lane 0's claim slots visible to the record build
             }
             if (worth) {
               const uint32_t half = pend / 2;
@@ -1391,11 +1377,15 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
     a.task_stride = (unsigned long long)cfg->shard_count;
     a.l1_offset = 0;
     a.l1_stride = 1;
+    a.shard_level = 1;
   } else {
     a.task_offset = 0;
     a.task_stride = 1;
     a.l1_offset = (uint32_t)cfg->shard_rank;
     a.l1_stride = (uint32_t)cfg->shard_count;
+    // WM_MOTIF_SHARD_LEVEL=1|2 overrides (A/B); default level 2 from k = 6
+    const char *sl = getenv("WM_MOTIF_SHARD_LEVEL");
+    a.shard_level = (sl && (*sl == '1' || *sl == '2')) ? (*sl - '0') : (k >= 6 ? 2 : 1);
   }
   a.ntasks = ntask > a.task_offset ? (ntask - a.task_offset + a.task_stride - 1) / a.task_stride : 0;
   a.k = k;

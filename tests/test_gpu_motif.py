@@ -141,6 +141,29 @@ def test_root_suffix_and_shards(cuda):
     assert [sum(x) for x in zip(*parts)] == full
 
 
+@pytest.mark.parametrize("level", ["1", "2"])
+def test_shards_partition_deep_motifs(scale_golden, cuda, monkeypatch, level):
+    """k = 6 / 7 shards (level-1 edge tasks or level-2 (root, child,
+    grandchild) tasks, WM_MOTIF_SHARD_LEVEL) partition the tree: their
+    histograms sum to the golden one, with and without forced balancing."""
+    from paper_2212_04551_b200 import BalanceConfig, run_motifs, synth
+    monkeypatch.setenv("WM_MOTIF_SHARD_LEVEL", level)
+    lb = BalanceConfig(threshold=1.0, poll_interval=1)
+    g = synth.config_graph("cfg2")
+    for k in (6, 7) if "7" in scale_golden["cfg2"]["motif"] else (6,):
+        want = scale_golden["cfg2"]["motif"][str(k)]["hist"]
+        for n in (2, 5):
+            parts = [run_motifs(g, k, dictionary(k), mode="opt", balance_config=lb,
+                                shard=(r, n), reduce=False).pattern_counts for r in range(n)]
+            assert [sum(x) for x in zip(*parts)] == want, (k, n)
+    g4 = synth.config_graph("cfg4")
+    want = scale_golden["cfg4"]["motif_suffix"]["k6_s4096"]["hist"]
+    parts = [run_motifs(g4, 6, dictionary(6), mode="opt", balance_config=lb,
+                        roots=(g4.n - 4096, g4.n), shard=(r, 4), reduce=False).pattern_counts
+             for r in range(4)]
+    assert [sum(x) for x in zip(*parts)] == want
+
+
 def test_cfg5_rmat_s22_root_suffix(scale_golden, cuda):
     """Config 5 (R-MAT scale 22): k=5/6/7 motif histograms over root suffixes
     (the induced subgraph on the last s ids) vs the pinned restatement."""
