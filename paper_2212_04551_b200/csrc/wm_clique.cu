@@ -1828,6 +1828,9 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   dnbr_p = g->ws->dag_nbr.as<int32_t>();
   }  // per-run path
   if ((st = g->ws->arena.ensure(sizeof(uint32_t) * (arena_words + 1)))) return st;
+  if (pt.on)
+    fprintf(stderr, "[wm phases] tasks by width (d<=32,64,128,256,512,1024,wide): %llu %llu "
+            "%llu %llu %llu %llu %llu\n", hb[0], hb[1], hb[2], hb[3], hb[4], hb[5], hb[6]);
 
   // width classes, contiguous in the descending sort: 32, 16, 8, then <= 4
   struct Cls { int wmax; unsigned long long begin, cnt; EnumPlan plan; };

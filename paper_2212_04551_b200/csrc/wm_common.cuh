@@ -160,35 +160,6 @@ __device__ __forceinline__ bool edge_hash_contains(const EdgeHash &H, int32_t u,
   }
 }
 
-// Two-phase probe: eh_issue loads the first bucket (no dependence on any
-// other probe), eh_resolve finishes it (rarely loading further buckets).
-// Issuing several probes before resolving any keeps their DRAM/L2 round trips
-// in flight together instead of one after another.
-struct EhProbe {
-  unsigned long long key;
-  ulonglong2 p, q;
-};
-
-__device__ __forceinline__ void eh_issue(const EdgeHash &H, int32_t u, int32_t v, EhProbe &pr) {
-  pr.key = eh_key(u, v);
-  const unsigned long long b = eh_bucket(pr.key, H.bmask);
-  pr.p = __ldg(H.b + 2 * b);
-  pr.q = __ldg(H.b + 2 * b + 1);
-}
-
-__device__ __forceinline__ bool eh_resolve(const EdgeHash &H, const EhProbe &pr) {
-  const unsigned long long key = pr.key;
-  if (pr.p.x == key || pr.p.y == key || pr.q.x == key || pr.q.y == key) return true;
-  if (pr.q.y == kEhEmpty) return false;
-  unsigned long long b = (eh_bucket(key, H.bmask) + 1) & H.bmask;  // overflow: keep probing
-  for (;;) {
-    const ulonglong2 p = __ldg(H.b + 2 * b), q = __ldg(H.b + 2 * b + 1);
-    if (p.x == key || p.y == key || q.x == key || q.y == key) return true;
-    if (q.y == kEhEmpty) return false;
-    b = (b + 1) & H.bmask;
-  }
-}
-
 using aref_u64 = cuda::atomic_ref<unsigned long long, cuda::thread_scope_device>;
 using aref_i32 = cuda::atomic_ref<int, cuda::thread_scope_device>;
 using aref_u32 = cuda::atomic_ref<uint32_t, cuda::thread_scope_device>;

@@ -170,22 +170,10 @@ __device__ __forceinline__ bool adj_tr(const MotifArgs &a, const MotifWarp &w, i
 __device__ __forceinline__ bool adj_none(const MotifArgs &a, const MotifWarp &w, int L, int32_t e) {
   if (a.H.b) {
     bool hit = false;
-#if WM_EH_2PHASE
-    // all first-bucket loads issued before any is resolved
-    EhProbe pr[WM_EH_2PHASE];
-#pragma unroll
-    for (int j = 0; j < WM_EH_2PHASE; ++j)
-      if (j < L) eh_issue(a.H, e, w.tr[j], pr[j]);
-#pragma unroll
-    for (int j = 0; j < WM_EH_2PHASE; ++j)
-      if (j < L) hit |= eh_resolve(a.H, pr[j]);
-    for (int j = WM_EH_2PHASE; j < L; ++j) hit |= edge_hash_contains(a.H, e, w.tr[j]);
-#else
 #pragma unroll
     for (int j = 0; j < WM_BPART_UNROLL; ++j)
       if (j < L) hit |= edge_hash_contains(a.H, e, w.tr[j]);
     for (int j = WM_BPART_UNROLL; j < L; ++j) hit |= edge_hash_contains(a.H, e, w.tr[j]);
-#endif
     return !hit;
   }
   bool keep = true;
