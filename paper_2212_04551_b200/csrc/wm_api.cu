@@ -208,14 +208,14 @@ __global__ void csr_check_kernel(int64_t n, int64_t nnz, const int64_t *__restri
             int64_t lo = off[v], hi = off[v + 1];
             if (lo < 0) lo = 0;
             if (hi > nnz) hi = nnz;
-            bool found = false;
-            while (lo < hi) {
-              const int64_t mid = (lo + hi) >> 1;
-              const int32_t y = nbr[mid];
-              if (y == (int32_t)u) { found = true; break; }
-              if (y < (int32_t)u) lo = mid + 1; else hi = mid;
-            }
-            if (!found) k = ((unsigned long long)u << 33) | (kCsrSym << 31) | (unsigned long long)v;
+            // interpolation + binary search (a hub row of 41K ids: ~5 loads);
+            // a miss is re-checked by a linear scan, so an unsorted row of v
+            // (reported at v) never masquerades as an asymmetric edge here —
+            // the reference tests membership in a set (graph.py:132-133)
+            bool found = lo < hi && row_contains(nbr, lo, hi, (int32_t)u);
+            for (int64_t q = lo; q < hi && !found; ++q) found = nbr[q] == (int32_t)u;
+            if (!found)
+              k = ((unsigned long long)u << 33) | (kCsrSym << 31) | (unsigned long long)v;
           }
         }
 #pragma unroll

@@ -4,7 +4,8 @@ and device time.  With one process per GPU the N-GPU step time is the slowest
 shard, so t(N=1) / max_r t_r is the speed-up the sharding allows (the
 measured multi-GPU numbers come from bench.py --gpus N under torchrun).
 
-    python scripts/shard_scaling.py > profiles/rNN_shard_scaling.jsonl
+    python scripts/shard_scaling.py [cfg3:8 cfg5:12 motif:cfg5:7:32768 ...] \
+        > profiles/rNN_shard_scaling.jsonl
 """
 import json
 import sys
@@ -24,10 +25,10 @@ def best(fn, reps=3):
     return out
 
 
-def sweep(name, fn, count):
+def sweep(name, fn, count, reps=3):
     base = None
     for N in (1, 2, 4, 8):
-        rs = [best(lambda: fn((r, N))) for r in range(N)]
+        rs = [best(lambda: fn((r, N)), reps) for r in range(N)]
         tot = sum(count(x) for x in rs)
         kmax = max(x.kernel_ms for x in rs)
         dmax = max(x.device_ms for x in rs)
@@ -41,13 +42,21 @@ def sweep(name, fn, count):
             "efficiency_device": base[1] / dmax / N}), flush=True)
 
 
-g3 = synth.config_graph("cfg3")
-sweep("cfg3 clique k=8", lambda sh: run_clique(g3, 8, mode="opt", balance_config=CL, shard=sh,
-                                               reduce=False), lambda r: r.clique_count)
-g5 = synth.config_graph("cfg5")
-sweep("cfg5 clique k=8", lambda sh: run_clique(g5, 8, mode="opt", balance_config=CL, shard=sh,
-                                               reduce=False), lambda r: r.clique_count)
-d7 = build_dictionary(7)
-sweep("cfg5 motif k=7 root suffix 32768",
-      lambda sh: run_motifs(g5, 7, d7, mode="opt", balance_config=MO, roots=(g5.n - 32768, g5.n),
-                            shard=sh, reduce=False), lambda r: r.aggregated_total)
+WORKLOADS = sys.argv[1:] or ["cfg3:8", "cfg3:9", "cfg3:10", "cfg5:8", "cfg5:12",
+                             "motif:cfg5:7:32768"]
+for wl in WORKLOADS:
+    parts = wl.split(":")
+    if parts[0] == "motif":
+        g = synth.config_graph(parts[1])
+        k, suf = int(parts[2]), int(parts[3])
+        d = build_dictionary(k)
+        sweep("%s motif k=%d root suffix %d" % (parts[1], k, suf),
+              lambda sh: run_motifs(g, k, d, mode="opt", balance_config=MO,
+                                    roots=(g.n - suf, g.n), shard=sh, reduce=False),
+              lambda r: r.aggregated_total)
+    else:
+        g = synth.config_graph(parts[0])
+        k = int(parts[1])
+        sweep("%s clique k=%d" % (parts[0], k),
+              lambda sh: run_clique(g, k, mode="opt", balance_config=CL, shard=sh, reduce=False),
+              lambda r: r.clique_count, reps=3 if k <= 10 else 1)

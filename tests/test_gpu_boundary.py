@@ -90,6 +90,17 @@ def test_first_violation_in_reference_order(cuda):
         _create_host(n, off, nbr)
 
 
+def test_unsorted_row_reported_at_its_vertex(cuda):
+    """Row 2 unsorted but symmetric: the reference's set-membership symmetry
+    check passes at vertices 0 and 1 and the ascending check fails at 2."""
+    rows = [[1, 2], [0, 2], [1, 0]]
+    off = np.cumsum([0] + [len(r) for r in rows])
+    with pytest.raises(ValueError, match="adjacency of 2 not strictly ascending"):
+        _create_host(3, off, sum(rows, []))
+    with pytest.raises(ValueError, match="adjacency of 2 not strictly ascending"):
+        _create_device(3, off, sum(rows, []))
+
+
 def test_good_graphs_accepted(cuda):
     from paper_2212_04551_b200 import gnp_random_graph, run_clique, synth
     g = gnp_random_graph(200, 0.1, 5)
