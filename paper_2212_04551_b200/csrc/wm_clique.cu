@@ -212,6 +212,7 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
                                                            unsigned long long ntask,
                                                            const unsigned long long *__restrict__ bm_off,
                                                            uint32_t *__restrict__ bm,
+                                                           unsigned long long below,
                                                            unsigned long long first,
                                                            unsigned long long stride,
                                                            const int64_t *__restrict__ goff,
@@ -220,10 +221,12 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
   BuildSmem<W> &sm = reinterpret_cast<BuildSmem<W> *>(smraw)[threadIdx.x >> 5];
   const int lane = lane_id();
   const unsigned long long nwarps = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
-  // only this shard's tasks (first + j * stride) need a bitmap
-  for (unsigned long long t = first + stride * (((unsigned long long)blockIdx.x * blockDim.x +
-                                                 threadIdx.x) >> 5);
-       t < ntask; t += nwarps * stride) {
+  // only this shard's tasks need a bitmap: every t < below (split over the
+  // shards at level 1), then t = first + j * stride
+  const unsigned long long wid = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const unsigned long long nmine = below + (first < ntask ? (ntask - first + stride - 1) / stride : 0);
+  for (unsigned long long j = wid; j < nmine; j += nwarps) {
+    const unsigned long long t = j < below ? j : first + (j - below) * stride;
     const int32_t v = __ldg(tasks + t);
     const int64_t b = __ldg(doff + v);
     const int d = (int)(__ldg(doff + v + 1) - b);
@@ -336,6 +339,12 @@ struct CliqueArgs {
   unsigned long long ntasks;         // tasks of this shard in the class
   unsigned long long task_offset;    // shard rank
   unsigned long long task_stride;    // shard count
+  // multi-GPU: the class's first `heavy` (costliest) tasks are processed by
+  // EVERY shard, each over its own level-1 members (member i + task = rank
+  // mod N) — one hub root's subtree no longer lands on one GPU; the others are
+  // dealt whole, task index = rank (mod N), from rem_first on
+  unsigned long long heavy;
+  unsigned long long rem_first;
   int k;
   int lb_on;
   int lb_poll;
@@ -907,7 +916,7 @@ __device__ __noinline__
 #endif
 void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
                                       unsigned long long task, int s0, int32_t root, int d,
-                                      int64_t lb, const Rec3 &rec, bool stage,
+                                      int64_t lb, const Rec3 &rec, bool stage, bool split,
                                       TaskCounters &tcio) {
   constexpr int S = Width<w>::S;
   const int lane = lane_id();
@@ -946,6 +955,13 @@ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
         const int lo = lane * 32;
         cword = d >= lo + 32 ? 0xffffffffu : (d > lo ? (1u << (d - lo)) - 1u : 0u);
         pword = cword;
+        if (split) {  // this shard's level-1 members: (member + task) = rank (mod N)
+          uint32_t mine = 0u;
+          const unsigned long long N = a.task_stride;
+          for (int j = 0; j < 32; ++j)
+            mine |= (((unsigned long long)(lo + j) + task) % N == a.task_offset ? 1u : 0u) << j;
+          pword &= mine;
+        }
       } else {
         cword = cv;
         pword = pv;
@@ -1104,10 +1120,17 @@ __global__ void __launch_bounds__(256, WMAX <= 4 ? WM_ENUM_MINBLOCKS : 1)
     if (kind == 0) break;
     unsigned long long task;
     int s0;
+    bool split = false;
     if (kind == 1) {
-      task = a.task_offset + ti * a.task_stride;
+      if (ti < a.heavy) {
+        task = ti;
+        split = true;
+        tasks_done += (task % a.task_stride == a.task_offset);  // count each task once
+      } else {
+        task = a.rem_first + (ti - a.heavy) * a.task_stride;
+        ++tasks_done;
+      }
       s0 = 1;
-      ++tasks_done;
     } else {
       task = __shfl_sync(0xffffffffu, rec.w[0], 0);
       s0 = (int)__shfl_sync(0xffffffffu, rec.w[0], 1);
@@ -1119,11 +1142,11 @@ __global__ void __launch_bounds__(256, WMAX <= 4 ? WM_ENUM_MINBLOCKS : 1)
     cached = task;
     const int wv = (d + 31) >> 5;
     if (WMAX <= 4) {
-      if (wv <= 1) run_task<1, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, tc);
-      else if (wv <= 2) run_task<(WMAX >= 2 ? 2 : 1), WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, tc);
-      else run_task<WMAX, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, tc);
+      if (wv <= 1) run_task<1, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, split, tc);
+      else if (wv <= 2) run_task<(WMAX >= 2 ? 2 : 1), WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, split, tc);
+      else run_task<WMAX, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, split, tc);
     } else {
-      run_task<WMAX, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, tc);
+      run_task<WMAX, WMAX, BYTES>(sm, a, kind, task, s0, root, d, lb, rec, stage, split, tc);
     }
   }
   const unsigned long long acc = warp_sum_u64(tc.acc);
@@ -1254,8 +1277,8 @@ static int run_clique_dfs(Graph *g, const wm_cfg *cfg, int k, unsigned long long
 
 template <int W>
 static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask,
-                        unsigned long long first, unsigned long long stride, int order,
-                        int rank_order, cudaStream_t s) {
+                        unsigned long long all_below, unsigned long long first,
+                        unsigned long long stride, int order, int rank_order, cudaStream_t s) {
   const size_t per_warp = sizeof(BuildSmem<W>);
   int wpb = 8;
   while (wpb > 1 && per_warp * wpb > 200 * 1024) wpb >>= 1;
@@ -1266,12 +1289,14 @@ static int launch_build(Graph *g, const CliqueArgs &a, unsigned long long ntask,
   WM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
   if (bps < 1) return fail(WM_ECAPACITY, "clique build kernel W=%d does not fit on an SM", W);
   unsigned long long blocks = (unsigned long long)g->num_sms * bps;
-  const unsigned long long mine = first < ntask ? (ntask - first + stride - 1) / stride : 0;
+  const unsigned long long below = all_below < ntask ? all_below : ntask;
+  const unsigned long long mine =
+      below + (first < ntask ? (ntask - first + stride - 1) / stride : 0);
   if (!mine) return WM_OK;
   const unsigned long long need = (mine + wpb - 1) / wpb;
   if (blocks > need) blocks = need;
   kern<<<(int)blocks, wpb * 32, smem, s>>>(a.doff, a.dnbr, a.tasks, ntask, a.bm_off,
-                                           const_cast<uint32_t *>(a.bm), first, stride,
+                                           const_cast<uint32_t *>(a.bm), below, first, stride,
                                            g->offsets, order, rank_order);
   WM_CUDA(cudaGetLastError());
   return WM_OK;
@@ -1833,24 +1858,40 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
             "%llu %llu %llu %llu %llu\n", hb[0], hb[1], hb[2], hb[3], hb[4], hb[5], hb[6]);
 
   // width classes, contiguous in the descending sort: 32, 16, 8, then <= 4
-  struct Cls { int wmax; unsigned long long begin, cnt; EnumPlan plan; };
+  struct Cls { int wmax; unsigned long long begin, cnt, heavy; EnumPlan plan; };
   Cls cls[4];
   int ncls = 0;
   {
     unsigned long long begin = 0;
     for (int c = 5; c >= 3; --c) {
-      if (hb[c]) cls[ncls++] = Cls{1 << c, begin, hb[c], EnumPlan()};
+      if (hb[c]) cls[ncls++] = Cls{1 << c, begin, hb[c], 0, EnumPlan()};
       begin += hb[c];
     }
     const unsigned long long small = hb[0] + hb[1] + hb[2];
-    if (small) cls[ncls++] = Cls{4, begin, small, EnumPlan()};
+    if (small) cls[ncls++] = Cls{4, begin, small, 0, EnumPlan()};
   }
+  // multi-GPU: each class's costliest tasks are split over all shards at
+  // level 1 (CliqueArgs::heavy); WM_CLIQUE_SPLIT = tasks per shard (default 32).
+  // Not for k = 3 (bulk2 roots have no level to split) or the B_alg pass.
+  const unsigned long long N = (unsigned long long)cfg->shard_count;
+  const unsigned long long R = (unsigned long long)cfg->shard_rank;
+  {
+    const char *sp = getenv("WM_CLIQUE_SPLIT");
+    const unsigned long long per = sp ? strtoull(sp, nullptr, 10) : 32ull;
+    for (int i = 0; i < ncls; ++i)
+      cls[i].heavy = (N > 1 && k >= 4 && !bytes) ? (cls[i].cnt < per * N ? cls[i].cnt : per * N)
+                                                  : 0ull;
+  }
+  // this shard's tasks of a class: all `heavy` (split), then index = R (mod N)
+  auto rem_first = [&](unsigned long long heavy) { return heavy + (R + N - heavy % N) % N; };
+  auto shard_tasks = [&](unsigned long long cnt, unsigned long long heavy) {
+    const unsigned long long f = rem_first(heavy);
+    return heavy + (cnt > f ? (cnt - f + N - 1) / N : 0ull);
+  };
   // plan + allocate everything before the timed region
   int max_warps = 0;
   for (int i = 0; i < ncls; ++i) {
-    const unsigned long long cnt = cls[i].cnt;
-    const unsigned long long ro = (unsigned long long)cfg->shard_rank;
-    const unsigned long long nt = cnt > ro ? (cnt - ro + cfg->shard_count - 1) / cfg->shard_count : 0;
+    const unsigned long long nt = shard_tasks(cls[i].cnt, cls[i].heavy);
     switch (cls[i].wmax) {
 #define WM_PLAN(WW)                                                                 \
   case WW:                                                                          \
@@ -1892,17 +1933,21 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
       a.bm = g->ws->arena.as<uint32_t>();
       begin += cnt;
       // arena offsets cover every task (shard-independent); only this shard's
-      // tasks are built: class-local index (class_off + t) = rank (mod N)
+      // tasks are built: the class's split tasks (class-local index < heavy)
+      // and class-local index (class_off + t) = rank (mod N) above them
       unsigned long long class_off = 0;
       for (int c2 = 2; c2 > c; --c2) class_off += hb[c2];  // buckets 0-2 share a class
       if (c > 2) class_off = 0;
-      const unsigned long long N = (unsigned long long)cfg->shard_count;
-      const unsigned long long first =
-          ((unsigned long long)cfg->shard_rank + N - class_off % N) % N;
+      unsigned long long heavy_c = 0;
+      for (int i = 0; i < ncls; ++i)
+        if (cls[i].wmax == (c > 2 ? (1 << c) : 4)) heavy_c = cls[i].heavy;
+      const unsigned long long all_below = heavy_c > class_off ? heavy_c - class_off : 0ull;
+      unsigned long long first = (R + N - class_off % N) % N;  // t = first (mod N)
+      if (first < all_below) first += (all_below - first + N - 1) / N * N;
       switch (c) {
 #define WM_BCASE(CC, WW) \
   case CC:               \
-    st = launch_build<WW>(g, a, cnt, first, N, order, !bytes, s); \
+    st = launch_build<WW>(g, a, cnt, all_below, first, N, order, !bytes, s); \
     break;
         WM_BCASE(0, 1) WM_BCASE(1, 2) WM_BCASE(2, 4) WM_BCASE(3, 8) WM_BCASE(4, 16)
         WM_BCASE(5, 32)
@@ -1918,11 +1963,11 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
       a.tasks = tasks_sorted + cls[i].begin;
       a.bm_off = bm_off + cls[i].begin;
       a.bm = g->ws->arena.as<uint32_t>();
-      a.task_offset = (unsigned long long)cfg->shard_rank;
-      a.task_stride = (unsigned long long)cfg->shard_count;
-      const unsigned long long cnt = cls[i].cnt;
-      a.ntasks =
-          cnt > a.task_offset ? (cnt - a.task_offset + a.task_stride - 1) / a.task_stride : 0;
+      a.task_offset = R;
+      a.task_stride = N;
+      a.heavy = cls[i].heavy;
+      a.rem_first = rem_first(cls[i].heavy);
+      a.ntasks = shard_tasks(cls[i].cnt, cls[i].heavy);
       a.k = k;
       a.lb_on = lb_on;
       a.lb_poll = cfg->lb_poll > 0 ? cfg->lb_poll : 1;

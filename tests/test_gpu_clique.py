@@ -113,6 +113,30 @@ def test_sharded_runs_sum_to_total(cuda):
         assert sum(parts) == total
 
 
+@pytest.mark.parametrize("split", ["0", "1", "32", "1000000"])
+def test_split_heavy_tasks_partition(scale_golden, cuda, monkeypatch, split):
+    """The costliest tasks of each width class are split over all shards at
+    level 1 (WM_CLIQUE_SPLIT per shard; 0 = whole-task dealing only): shard
+    counts sum to the golden total for every split size, and every task is
+    counted once."""
+    from paper_2212_04551_b200 import BalanceConfig, run_clique, synth
+    monkeypatch.setenv("WM_CLIQUE_SPLIT", split)
+    g = synth.config_graph("cfg3")
+    lb = BalanceConfig(threshold=1.0)
+    single = run_clique(g, 6, mode="opt", balance_config=lb)
+    assert single.clique_count == scale_golden["cfg3"]["clique"]["6"]["count"]
+    for n in (3, 8):
+        rs = [run_clique(g, 6, mode="opt", balance_config=lb, shard=(r, n), reduce=False)
+              for r in range(n)]
+        assert sum(r.clique_count for r in rs) == single.clique_count, (split, n)
+        assert sum(r.tasks for r in rs) == single.tasks
+    # k = 4 with the id orientation (wider roots: the W > 4 classes)
+    want = run_clique(g, 4, order="id").clique_count
+    parts = [run_clique(g, 4, order="id", shard=(r, 4), reduce=False).clique_count
+             for r in range(4)]
+    assert sum(parts) == want == scale_golden["cfg3"]["clique"]["4"]["count"]
+
+
 def test_root_range_is_induced_suffix(cuda):
     """roots=(r0, n) in id order enumerates exactly the induced subgraph on
     [r0, n) (reference roots ascend, engine.py:187)."""
