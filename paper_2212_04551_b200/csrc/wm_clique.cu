@@ -956,10 +956,11 @@ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
         cword = d >= lo + 32 ? 0xffffffffu : (d > lo ? (1u << (d - lo)) - 1u : 0u);
         pword = cword;
         if (split) {  // this shard's level-1 members: (member + task) = rank (mod N)
+          const uint32_t N = (uint32_t)a.task_stride;
+          const uint32_t base = (uint32_t)(((unsigned long long)lo + task) % N);
           uint32_t mine = 0u;
-          const unsigned long long N = a.task_stride;
-          for (int j = 0; j < 32; ++j)
-            mine |= (((unsigned long long)(lo + j) + task) % N == a.task_offset ? 1u : 0u) << j;
+          for (uint32_t j = ((uint32_t)a.task_offset + N - base) % N; j < 32u; j += N)
+            mine |= 1u << j;
           pword &= mine;
         }
       } else {
@@ -1101,8 +1102,13 @@ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
 #ifndef WM_ENUM_MINBLOCKS
 #define WM_ENUM_MINBLOCKS 5
 #endif
+// (W = 8: <= 128 registers keeps two blocks per SM)
+#ifndef WM_ENUM_MINBLOCKS_W8
+#define WM_ENUM_MINBLOCKS_W8 2
+#endif
 template <int WMAX, bool BYTES>
-__global__ void __launch_bounds__(256, WMAX <= 4 ? WM_ENUM_MINBLOCKS : 1)
+__global__ void __launch_bounds__(256, WMAX <= 4 ? WM_ENUM_MINBLOCKS
+                                                 : (WMAX == 8 ? WM_ENUM_MINBLOCKS_W8 : 1))
     clique_enum_kernel(CliqueArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   CliqueSmem<WMAX> &sm = reinterpret_cast<CliqueSmem<WMAX> *>(smraw)[threadIdx.x >> 5];

@@ -1,4 +1,4 @@
-"""A/B timing of clique kernel builds: python scripts/ab_clique.py K lib1.so lib2.so ...
+"""A/B timing of clique kernel builds: [WM_AB_CFG=cfg5] python scripts/ab_clique.py K lib1.so ...
 Each library runs in a fresh process (WM_B200_LIB); prints median kernel ms."""
 import json
 import os
@@ -10,10 +10,10 @@ if len(sys.argv) > 2 and sys.argv[1] == "--one":
     import statistics
     from paper_2212_04551_b200 import BalanceConfig, run_clique, synth
     k = int(sys.argv[2])
-    g = synth.config_graph(sys.argv[3] if len(sys.argv) > 3 else "cfg3")
+    g = synth.config_graph(os.environ.get("WM_AB_CFG", "cfg3"))
     bc = BalanceConfig(threshold=1.0, poll_interval=int(os.environ.get("WM_POLL", "32")))
     ms = []
-    for i in range(6):
+    for i in range(int(os.environ.get("WM_AB_REPS", "6"))):
         r = run_clique(g, k, mode="opt", balance_config=bc)
         if i:
             ms.append(r.kernel_ms)
