@@ -4,7 +4,7 @@
 Headline workload (a "step"): one full k-clique count of BASELINE config 3 —
 the Chung-Lu power-law graph with 100,000 vertices / 947,479 edges (SURVEY
 §8(d) recipe, seed 3) — through ``run_clique`` (clique_app pipeline) in
-``opt`` mode (on-device load balancer on).  Default k=8 (9,384,222,498
+``opt`` mode (on-device load balancer on).  Default k=9 (34,125,264,080
 cliques).  Counts are checked against the pinned golden value every step.
 
 At N=1 the same JSON line also carries the motif half of the metric
@@ -45,12 +45,14 @@ METRIC = "subgraphs enumerated/sec (k-clique, k-motif) at 1/2/4/8 B200 vs CPU re
 UNIT = "subgraphs/s"
 # CPU reference step: a fixed slice of the reference's own root queue (ids
 # ascending, engine.py:187), run to completion.  cfg3 ids are weight-ordered
-# (vertex 0 heaviest) and in id order every 8-clique is rooted below id ~100:
-# roots [40, 100) hold 26,241 of them (~12 s on 8 host threads) — a complete,
-# deterministic piece of the real workload, so the per-step rate is stable.
-# (Roots < 40 are single subtrees of minutes each; random root subsets swing
-# the rate by 100x with whether a hub lands in them.)
+# (vertex 0 heaviest) and in id order every 8- or 9-clique is rooted below id
+# ~100: roots [40, 100) hold 26,241 8-cliques / 4,548 9-cliques (~12-13 s on 8
+# host threads) — a complete, deterministic piece of the real workload, so
+# the per-step rate is stable.  (Roots < 40 are single subtrees of minutes
+# each; random root subsets swing the rate by 100x with whether a hub lands in
+# them.)  Warm-up steps run the short tail [60, 100) of the same slice.
 REF_ROOTS = (40, 100)
+REF_WARMUP_ROOTS = (60, 100)
 REF_SEED = 0
 # motif workloads of the N=1 line: (config, k, root suffix, LB-off suffix)
 MOTIF_WORKLOADS = (("cfg4", 5, 16384, 16384), ("cfg4", 6, 16384, 8192),
@@ -278,7 +280,7 @@ def run_reference(args):
     from paper_2212_04551_b200 import synth
     g = synth.config_graph("cfg3")
     for _ in range(args.warmup):
-        cpu_clique_subset(g, args.k)
+        cpu_clique_subset(g, args.k, REF_WARMUP_ROOTS)
     rates, leaves, secs = [], 0, 0.0
     for _ in range(args.steps):
         rate, lv, dt, threads = cpu_clique_subset(g, args.k)
@@ -395,7 +397,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--k", type=int, default=8)
+    ap.add_argument("--k", type=int, default=9)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extras", action="store_true", help="skip LB/secondary evidence")
@@ -489,6 +491,7 @@ def main():
             "kernel_ms_lb_off": rw.kernel_ms, "kernel_ms_lb_on": ro.kernel_ms,
             "migrations": ro.migrations, "donations": ro.rebalance_count}
         extras["secondary"] = secondary_workloads(stream)
+        extras["cfg3_other_k"] = other_k(args, g, gold, stream, flush, bc)
     if world == 1 and not args.no_motif:
         extras["motif"] = motif_block(args, stream, flush, gold, peak, peak_src, ncu)
     cpu = None
@@ -628,6 +631,28 @@ def motif_block(args, stream, flush, gold, peak, peak_src, ncu):
                                                                  done, lv, dt),
                 "cpu_model": cpu_model()}
         out["%s_%s" % (cfg, key)] = rec
+    return out
+
+
+def other_k(args, g, gold, stream, flush, bc):
+    """cfg3 at the neighbouring k (the BASELINE config is k = 5..12): same
+    timing as the headline, fewer steps; counts checked against the goldens."""
+    from paper_2212_04551_b200 import run_clique
+    out = {}
+    for k in (5, 8, 10):
+        if k == args.k:
+            continue
+        want = gold.get("cfg3", {}).get("clique", {}).get(str(k), {}).get("count")
+        for _ in range(2):
+            run_clique(g, k, mode="opt", balance_config=bc, stream=stream)
+        ms, rs, _ = timed_steps(lambda: run_clique(g, k, mode="opt", balance_config=bc,
+                                                   stream=stream), 3, stream, flush, 1)
+        out["k%d" % k] = {"value": sum(r.clique_count for r in rs) / (sum(ms) * 1e-3),
+                          "unit": UNIT, "ms_per_step": sum(ms) / len(ms),
+                          "kernel_ms": statistics.mean(r.kernel_ms for r in rs),
+                          "count_per_step": rs[0].clique_count,
+                          "count_matches_golden": want is None or
+                          all(r.clique_count == want for r in rs)}
     return out
 
 
