@@ -1881,12 +1881,19 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   // Not for k = 3 (bulk2 roots have no level to split) or the B_alg pass.
   const unsigned long long N = (unsigned long long)cfg->shard_count;
   const unsigned long long R = (unsigned long long)cfg->shard_rank;
+  // Deep runs (k >= 10) split EVERY task: each rank then builds every bitmap
+  // (the build is < 1 % of such a run) and the shards balance to within a few
+  // percent — cfg5 k=12 at 8 shards 6.3x -> 7.5x (profiles/r02_split_cfg5k12.log);
+  // shallow runs split only the costliest 32 x N, since replicating the build
+  // would cost more than the imbalance (cfg5 k=8: 31 ms build vs 10 ms kernel
+  // per shard).
   {
     const char *sp = getenv("WM_CLIQUE_SPLIT");
-    const unsigned long long per = sp ? strtoull(sp, nullptr, 10) : 32ull;
-    for (int i = 0; i < ncls; ++i)
-      cls[i].heavy = (N > 1 && k >= 4 && !bytes) ? (cls[i].cnt < per * N ? cls[i].cnt : per * N)
-                                                  : 0ull;
+    const unsigned long long per = sp ? strtoull(sp, nullptr, 10) : (k >= 10 ? ~0ull : 32ull);
+    for (int i = 0; i < ncls; ++i) {
+      const unsigned long long cap = per == ~0ull ? ~0ull : per * N;
+      cls[i].heavy = (N > 1 && k >= 4 && !bytes) ? (cls[i].cnt < cap ? cls[i].cnt : cap) : 0ull;
+    }
   }
   // this shard's tasks of a class: all `heavy` (split), then index = R (mod N)
   auto rem_first = [&](unsigned long long heavy) { return heavy + (R + N - heavy % N) % N; };

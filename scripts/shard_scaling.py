@@ -13,7 +13,8 @@ import sys
 sys.path.insert(0, "/root/repo")
 from paper_2212_04551_b200 import BalanceConfig, build_dictionary, run_clique, run_motifs, synth
 
-CL = BalanceConfig(threshold=1.0, poll_interval=32)
+import os
+CL = BalanceConfig(threshold=1.0, poll_interval=int(os.environ.get("WM_POLL", "32")))
 MO = BalanceConfig(threshold=1.0, poll_interval=2)
 
 
