@@ -382,6 +382,7 @@ struct Workspace {
   DeviceBuffer lb, ring, counters, hist, arena, table, listing, listing_ring;
   DeviceBuffer edge_src, edge_flag, edge_pos;  // clique orientation, per directed edge
   DeviceBuffer claims;  // motif B_alg claim slots (count_bytes with the balancer on)
+  DeviceBuffer ehash_local;  // motif root-suffix runs: edge hash of the induced subgraph
   cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
 };
 

@@ -39,24 +39,26 @@
 
 namespace wm {
 
-__global__ void degree_kernel(int64_t n, const int64_t *__restrict__ off,
-                              int32_t *__restrict__ deg) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x)
-    deg[v] = (int32_t)(off[v + 1] - off[v]);
-}
-
-// sort keys for root tasks: degree+1 inside the root range (deterministic)
-__global__ void motif_task_keys_kernel(int64_t n, const int32_t *__restrict__ deg, int64_t rb,
-                                       int64_t re, uint32_t *__restrict__ keys,
+// sort keys of the root range [rb, re) only (entry i = vertex rb + i):
+// degree + 1 for roots with an edge, 0 otherwise; warp-aggregated count
+__global__ void motif_task_keys_kernel(const int64_t *__restrict__ off, int64_t rb, int64_t re,
+                                       uint32_t *__restrict__ keys,
                                        int32_t *__restrict__ vals,
                                        unsigned long long *__restrict__ ntask) {
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const bool ok = v >= rb && v < re && deg[v] > 0;
-    keys[v] = ok ? (uint32_t)deg[v] + 1u : 0u;
-    vals[v] = (int32_t)v;
-    if (ok) atomicAdd(ntask, 1ull);
+  const int64_t R = re - rb;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i0 = (int64_t)blockIdx.x * blockDim.x; i0 < R; i0 += stride) {
+    const int64_t i = i0 + threadIdx.x;
+    bool ok = false;
+    if (i < R) {
+      const int64_t v = rb + i;
+      const int64_t d = off[v + 1] - off[v];
+      ok = d > 0;
+      keys[i] = ok ? (uint32_t)d + 1u : 0u;
+      vals[i] = (int32_t)v;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    if (lane_id() == 0 && bal) atomicAdd(ntask, (unsigned long long)__popc(bal));
   }
 }
 
@@ -997,14 +999,15 @@ __global__ void __launch_bounds__(256) motif_dfs_kernel(MotifArgs a) {
 
 // Edge hash set construction (see EdgeHash): one warp per vertex u inserts the
 // keys of its neighbours v > u with atomicCAS, slots in order within a bucket.
-__global__ void edge_hash_build_kernel(int64_t n, const int64_t *__restrict__ off,
+// every edge {u, v} with lo <= u < v (lo = 0: the whole graph)
+__global__ void edge_hash_build_kernel(int64_t lo, int64_t n, const int64_t *__restrict__ off,
                                        const int32_t *__restrict__ nbr,
                                        unsigned long long *__restrict__ keys,
                                        unsigned long long bmask) {
   const int lane = lane_id();
   const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = wid; u < n; u += nw) {
+  for (int64_t u = lo + wid; u < n; u += nw) {
     const int64_t b = off[u], e = off[u + 1];
     for (int64_t p = b + lane; p < e; p += 32) {
       const int32_t v = nbr[p];
@@ -1038,7 +1041,7 @@ int graph_edge_hash(Graph *g, cudaStream_t s) {
                              ? (g->n * 32 + 255) / 256
                              : (int64_t)g->num_sms * 16;
   edge_hash_build_kernel<<<(int)(blocks > 0 ? blocks : 1), 256, 0, s>>>(
-      g->n, g->offsets, g->neighbors, static_cast<unsigned long long *>(p), slots / 4 - 1);
+      0, g->n, g->offsets, g->neighbors, static_cast<unsigned long long *>(p), slots / 4 - 1);
   WM_CUDA(cudaGetLastError());
   g->ehash = static_cast<unsigned long long *>(p);
   g->ehash_bmask = slots / 4 - 1;
@@ -1318,7 +1321,6 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
     return fail(WM_EINVAL, "motif kernel packs vertex ids in %d bits; n=%lld too large for k=%d",
                 vbits, (long long)n, k);
   int st;
-  if ((st = g->ws->outdeg.ensure(sizeof(int32_t) * (n + 1)))) return st;
   if ((st = g->ws->keys_in.ensure(sizeof(uint32_t) * n))) return st;
   if ((st = g->ws->keys_out.ensure(sizeof(uint32_t) * n))) return st;
   if ((st = g->ws->vals_in.ensure(sizeof(int32_t) * n))) return st;
@@ -1348,20 +1350,31 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
                               sizeof(uint32_t) * app->dict_len, cudaMemcpyHostToDevice, s));
   }
   const int tpb = 256;
-  const int eblocks = (int)((n + tpb - 1) / tpb < (int64_t)g->num_sms * 16
-                                ? (n + tpb - 1) / tpb
-                                : (int64_t)g->num_sms * 16);
-  degree_kernel<<<eblocks, tpb, 0, s>>>(n, g->offsets, g->ws->outdeg.as<int32_t>());
   const int64_t rb = cfg->root_begin < 0 ? 0 : cfg->root_begin;
   const int64_t re = (cfg->root_end < 0 || cfg->root_end > n) ? n : cfg->root_end;
-  motif_task_keys_kernel<<<eblocks, tpb, 0, s>>>(n, g->ws->outdeg.as<int32_t>(), rb, re,
-                                                 g->ws->keys_in.as<uint32_t>(),
-                                                 g->ws->vals_in.as<int32_t>(), ctr + 8);
-  size_t tb = g->ws->cub_tmp.bytes;
-  WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
-      g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
-      g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)n, 0,
-      task_key_bits(g), s));
+  const int64_t nr = re > rb ? re - rb : 0;  // only the root range is keyed and sorted
+  const int rblocks = (int)((nr + tpb - 1) / tpb < (int64_t)g->num_sms * 16
+                                ? (nr + tpb - 1) / tpb
+                                : (int64_t)g->num_sms * 16);
+  if (nr > 0) {
+    motif_task_keys_kernel<<<rblocks, tpb, 0, s>>>(g->offsets, rb, re,
+                                                   g->ws->keys_in.as<uint32_t>(),
+                                                   g->ws->vals_in.as<int32_t>(), ctr + 8);
+    size_t tb = g->ws->cub_tmp.bytes;
+    WM_CUDA(cub::DeviceRadixSort::SortPairsDescending(
+        g->ws->cub_tmp.ptr, tb, g->ws->keys_in.as<uint32_t>(), g->ws->keys_out.as<uint32_t>(),
+        g->ws->vals_in.as<int32_t>(), g->ws->vals_out.as<int32_t>(), (int)nr, 0,
+        task_key_bits(g), s));
+  }
+  // a root suffix run touches only the induced subgraph on [rb, n): every
+  // traversal vertex exceeds its root (canon.py:190-210), so every adjacency
+  // probe is an edge of that subgraph.  Its edges get their own hash set, built
+  // here (inside the timed run): rows of [rb, n) hold at most 2x its edges.
+  int64_t span[2] = {0, 0};
+  if (rb > 0) {
+    WM_CUDA(cudaMemcpyAsync(&span[0], g->offsets + rb, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaMemcpyAsync(&span[1], g->offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s));
+  }
   pt.mark("task sort");
   unsigned long long ntask = 0;
   WM_CUDA(cudaMemcpyAsync(&ntask, ctr + 8, sizeof ntask, cudaMemcpyDeviceToHost, s));
@@ -1420,9 +1433,26 @@ int run_motif(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cu
   a.H.bmask = 0;
   // WM_NO_EDGE_HASH=1 forces the CSR binary-search probes (fallback-path tests)
   const char *no_hash = getenv("WM_NO_EDGE_HASH");
+  const char *no_local = getenv("WM_NO_LOCAL_HASH");  // A/B: global table for suffix runs
   if (cfg->mode != WM_MODE_DFS && !(no_hash && *no_hash == '1')) {
-    // built once per graph (first motif run), before the timed kernel
-    if (graph_edge_hash(g, s) == WM_OK) {
+    const unsigned long long local_m = (unsigned long long)(span[1] - span[0]) / 2;
+    if (rb > 0 && !(no_local && *no_local == '1') && 4 * local_m < (unsigned long long)g->nnz) {
+      unsigned long long slots = 64;
+      while (slots < 2 * local_m) slots <<= 1;  // load factor <= 1/2
+      if ((st = g->ws->ehash_local.ensure(slots * sizeof(unsigned long long)))) return st;
+      WM_CUDA(cudaMemsetAsync(g->ws->ehash_local.ptr, 0xFF, slots * sizeof(unsigned long long), s));
+      const int64_t lw = (n - rb) * 32;
+      const int64_t lblocks = (lw + 255) / 256 < (int64_t)g->num_sms * 16 ? (lw + 255) / 256
+                                                                          : (int64_t)g->num_sms * 16;
+      edge_hash_build_kernel<<<(int)(lblocks > 0 ? lblocks : 1), 256, 0, s>>>(
+          rb, n, g->offsets, g->neighbors, g->ws->ehash_local.as<unsigned long long>(),
+          slots / 4 - 1);
+      WM_CUDA(cudaGetLastError());
+      a.H.b = reinterpret_cast<const ulonglong2 *>(g->ws->ehash_local.ptr);
+      a.H.bmask = slots / 4 - 1;
+      res->launches += 1;
+    } else if (graph_edge_hash(g, s) == WM_OK) {
+      // the whole graph's table: built once per graph (first motif run)
       a.H.b = reinterpret_cast<const ulonglong2 *>(g->ehash);
       a.H.bmask = g->ehash_bmask;
     }

@@ -177,6 +177,23 @@ def test_cfg5_rmat_s22_root_suffix(scale_golden, cuda):
             assert r.pattern_counts == want["hist"], (key, mode)
 
 
+def test_suffix_local_hash_matches_global(scale_golden, cuda, monkeypatch):
+    """Root-suffix runs probe a per-run edge hash of the induced subgraph on
+    [begin, n); the whole-graph table (WM_NO_LOCAL_HASH=1) gives the same
+    histograms, with and without forced balancing."""
+    from paper_2212_04551_b200 import BalanceConfig, run_motifs, synth
+    g = synth.config_graph("cfg4")
+    lb = BalanceConfig(threshold=1.0, poll_interval=1)
+    for key in ("k5_s4096", "k6_s4096", "k7_s2048"):
+        want = scale_golden["cfg4"]["motif_suffix"][key]
+        k, s = want["k"], want["suffix"]
+        for local in ("0", "1"):
+            monkeypatch.setenv("WM_NO_LOCAL_HASH", local)
+            r = run_motifs(g, k, dictionary(k), mode="opt", balance_config=lb,
+                           roots=(g.n - s, g.n))
+            assert r.pattern_counts == want["hist"], (key, local)
+
+
 def test_csr_probe_fallback_matches(golden, cuda, monkeypatch):
     """Without the edge hash set (allocation failure path) the CSR binary-search
     probes give the same histograms."""
