@@ -100,15 +100,21 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        """Start sampling and wait (<= 3 s) for the first sample, so even a
+        short timed region is covered; samples before mark() are dropped."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.Q,
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 3.0:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
+        self.first = len(self.lines)
 
     def _read(self):
         for line in self.proc.stdout:
@@ -125,7 +131,10 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, mx, reasons = [], 0.0, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        # the samples taken while the timed region ran (plus the one just
+        # before it when the region is shorter than the sampling period)
+        lines = self.lines[max(0, self.first - 1):]
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -402,6 +411,8 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--no-extras", action="store_true", help="skip LB/secondary evidence")
     ap.add_argument("--no-motif", action="store_true", help="skip the motif block")
+    ap.add_argument("--no-roofline", action="store_true",
+                    help="skip the B_alg pass (ncu launch-list captures of the timed steps)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -466,7 +477,7 @@ def main():
     extras = {}
     achieved = None
     b_alg = None
-    if world == 1:
+    if world == 1 and not args.no_roofline:
         rb = run_clique(g, args.k, count_bytes=True, stream=stream)
         b_alg = rb.alg_bytes
         achieved = b_alg / (kmean * 1e-3) / 1e9
