@@ -173,61 +173,69 @@ int red_edges(const wm_cfg *cfg, cudaStream_t s, const int64_t *nnz) {
 }
 
 // ---------------------------------------------------------------------------
-// CsrGraph.validate (graph.py:122-133) on the device, warp per vertex.  The
-// first violation in the reference's check order wins: vertex u ascending,
-// then per u: range/offsets, strictly ascending, self-loop, symmetry (first v
-// in row order).  Key = u << 33 | code << 31 | detail; atomicMin.  Offsets
-// that decrease are reported first (the reference checks them before any row,
-// graph.py:124-125): their own word, bad[1] = min vertex.
+// CsrGraph.validate (graph.py:122-133) on the device, one thread per stored
+// entry (hub rows spread over the grid).  The first violation in the
+// reference's check order wins: vertex u ascending, then per u: range,
+// strictly ascending, self-loop, symmetry (first v in row order).  Key =
+// u << 33 | code << 31 | detail; atomicMin.  Offsets that decrease are
+// reported first (the reference checks them before any row, graph.py:124-125):
+// their own word.  Symmetry is searched only for entries (u, v) with v > u;
+// with rows strictly ascending, "every such entry has its reverse" plus
+// "#(v > u) == #(v < u)" is symmetry.  Only an invalid graph gets a second
+// pass over the v < u entries (to name the first offending edge).
 enum : unsigned long long { kCsrRange = 0, kCsrAscend = 1, kCsrLoop = 2, kCsrSym = 3 };
 
+__global__ void csr_offsets_kernel(int64_t n, int64_t nnz, const int64_t *__restrict__ off,
+                                   unsigned long long *__restrict__ bad_off) {
+  for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
+       u += (int64_t)gridDim.x * blockDim.x)
+    if (off[u + 1] < off[u] || off[u] < 0 || off[u + 1] > nnz)
+      atomicMin(bad_off, (unsigned long long)u);
+}
+
+// bad[0] first violation key, bad[2] / bad[3] entries with v > u / v < u
 __global__ void csr_check_kernel(int64_t n, int64_t nnz, const int64_t *__restrict__ off,
-                                 const int32_t *__restrict__ nbr,
+                                 const int32_t *__restrict__ nbr, int lower_pass,
                                  unsigned long long *__restrict__ bad) {
-  const int lane = lane_id();
-  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  for (int64_t u = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; u < n; u += nw) {
-    int64_t b = off[u], e = off[u + 1];
-    unsigned long long key = ~0ull;
-    if (e < b || b < 0 || e > nnz) {
-      if (lane == 0) atomicMin(bad + 1, (unsigned long long)u);
-    } else {
-      for (int64_t p0 = b; p0 < e; p0 += 32) {
-        const int64_t p = p0 + lane;
-        unsigned long long k = ~0ull;
-        if (p < e) {
-          const int32_t v = nbr[p];
-          const unsigned long long det = (unsigned long long)(p - b + 1) & 0x7FFFFFFFull;
-          if (v < 0 || v >= n) {
-            k = ((unsigned long long)u << 33) | (kCsrRange << 31) | det;
-          } else if (p > b && nbr[p - 1] >= v) {
-            k = ((unsigned long long)u << 33) | (kCsrAscend << 31);
-          } else if (v == u) {
-            k = ((unsigned long long)u << 33) | (kCsrLoop << 31);
-          } else {
-            int64_t lo = off[v], hi = off[v + 1];
-            if (lo < 0) lo = 0;
-            if (hi > nnz) hi = nnz;
-            // interpolation + binary search (a hub row of 41K ids: ~5 loads);
-            // a miss is re-checked by a linear scan, so an unsorted row of v
-            // (reported at v) never masquerades as an asymmetric edge here —
-            // the reference tests membership in a set (graph.py:132-133)
-            bool found = lo < hi && row_contains(nbr, lo, hi, (int32_t)u);
-            for (int64_t q = lo; q < hi && !found; ++q) found = nbr[q] == (int32_t)u;
-            if (!found)
-              k = ((unsigned long long)u << 33) | (kCsrSym << 31) | (unsigned long long)v;
-          }
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const unsigned long long y = __shfl_xor_sync(0xffffffffu, k, o);
-          k = y < k ? y : k;
-        }
-        key = k < key ? k : key;
-        if (key != ~0ull) break;  // later positions of this row cannot win
-      }
+  unsigned long long up = 0, down = 0;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < nnz;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    // u = the row holding entry p: last u with off[u] <= p
+    int64_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (__ldg(off + mid) <= p) lo = mid; else hi = mid;
     }
-    if (lane == 0 && key != ~0ull) atomicMin(bad, key);
+    const int64_t u = lo, b = __ldg(off + u);
+    const int32_t v = __ldg(nbr + p);
+    unsigned long long k = ~0ull;
+    if (v < 0 || v >= n) {
+      k = ((unsigned long long)u << 33) | (kCsrRange << 31) |
+          ((unsigned long long)(p - b + 1) & 0x7FFFFFFFull);
+    } else if (p > b && __ldg(nbr + p - 1) >= v) {
+      k = ((unsigned long long)u << 33) | (kCsrAscend << 31);
+    } else if (v == u) {
+      k = ((unsigned long long)u << 33) | (kCsrLoop << 31);
+    } else if ((v > u) != (lower_pass != 0)) {
+      int64_t rl = __ldg(off + v), rh = __ldg(off + v + 1);
+      if (rl < 0) rl = 0;
+      if (rh > nnz) rh = nnz;
+      // interpolation + binary search (a hub row of 41K ids: ~5 loads); a
+      // miss is re-checked by a linear scan, so an unsorted row of v (reported
+      // at v) never masquerades as an asymmetric edge — the reference tests
+      // membership in a set (graph.py:132-133)
+      bool found = rl < rh && row_contains(nbr, rl, rh, (int32_t)u);
+      for (int64_t q = rl; q < rh && !found; ++q) found = __ldg(nbr + q) == (int32_t)u;
+      if (!found) k = ((unsigned long long)u << 33) | (kCsrSym << 31) | (unsigned long long)v;
+    }
+    if (v > (int32_t)u) ++up; else if (v < (int32_t)u) ++down;
+    if (k != ~0ull) atomicMin(bad, k);
+  }
+  up = warp_sum_u64(up);
+  down = warp_sum_u64(down);
+  if (lane_id() == 0 && !lower_pass) {
+    if (up) atomicAdd(bad + 2, up);
+    if (down) atomicAdd(bad + 3, down);
   }
 }
 
@@ -236,18 +244,29 @@ __global__ void csr_check_kernel(int64_t n, int64_t nnz, const int64_t *__restri
 static int csr_validate(Graph *g, cudaStream_t s) {
   int st = g->ws->counters.ensure(sizeof(unsigned long long) * 64);
   if (st) return st;
-  unsigned long long *bad = g->ws->counters.as<unsigned long long>() + 62;
+  unsigned long long *bad = g->ws->counters.as<unsigned long long>() + 58;  // [key, off, up, down]
   WM_CUDA(cudaMemsetAsync(bad, 0xff, 2 * sizeof(unsigned long long), s));
-  const int64_t want = (g->n * 32 + 255) / 256;
-  const int blocks = (int)(want < (int64_t)g->num_sms * 16 ? want : (int64_t)g->num_sms * 16);
-  csr_check_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(g->n, g->nnz, g->offsets,
-                                                           g->neighbors, bad);
-  WM_CUDA(cudaGetLastError());
-  unsigned long long hb[2] = {~0ull, ~0ull};
+  WM_CUDA(cudaMemsetAsync(bad + 2, 0, 2 * sizeof(unsigned long long), s));
+  const int64_t ns = (int64_t)g->num_sms;
+  const int vb = (int)((g->n + 255) / 256 < ns * 8 ? (g->n + 255) / 256 : ns * 8);
+  csr_offsets_kernel<<<vb > 0 ? vb : 1, 256, 0, s>>>(g->n, g->nnz, g->offsets, bad + 1);
+  unsigned long long hb[4] = {~0ull, ~0ull, 0, 0};
   WM_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
   if (hb[1] != ~0ull)
     return fail(WM_EINVAL, "offsets must be non-decreasing (vertex %lld)", (long long)hb[1]);
+  const int eb = (int)((g->nnz + 255) / 256 < ns * 32 ? (g->nnz + 255) / 256 : ns * 32);
+  for (int pass = 0; pass < 2; ++pass) {
+    if (g->nnz > 0)
+      csr_check_kernel<<<eb > 0 ? eb : 1, 256, 0, s>>>(g->n, g->nnz, g->offsets, g->neighbors,
+                                                       pass, bad);
+    WM_CUDA(cudaGetLastError());
+    WM_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaStreamSynchronize(s));
+    // a valid graph stops after pass 0; any violation also searches the
+    // v < u entries so the reported one is the first in the reference's order
+    if (hb[0] == ~0ull && hb[2] == hb[3]) break;
+  }
   const unsigned long long h = hb[0];
   if (h == ~0ull) return WM_OK;
   const long long u = (long long)(h >> 33);
