@@ -843,6 +843,33 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
   while (pc) {
     const int h = pop_hi(pc);
     const uint32_t ch = c & R[h];
+#ifndef WM_BULK5_WARPPUSH
+    // members are bit positions < 32, so lane i owns member i of ch: all the
+    // (h, i) pairs of the child at once, word_i = C_hi; each round every lane
+    // with j's left pushes one triple (ballot-compacted into the ring), so a
+    // child costs max_i |C_hi| rounds instead of one warp-wide trip per i
+    // (k=9 26.68 -> 26.46 ms, k=10 120.5 -> 118.6; profiles/r02_ab_lanepush.log;
+    // WM_BULK5_WARPPUSH=1 restores the per-i form)
+    uint32_t word = ((ch >> lane) & 1u) ? (ch & R[lane]) : 0u;
+    const uint32_t hi5 = ((uint32_t)h << 10) | ((uint32_t)lane << 5);
+    const uint32_t lt = (1u << lane) - 1u;
+    for (;;) {
+      const unsigned bal = __ballot_sync(0xffffffffu, word != 0u);
+      if (!bal) break;
+      if (word) {
+        const int j = pop_hi(word);
+        sm.queue[(head + nq + __popc(bal & lt)) & 63] = hi5 | (uint32_t)j;
+      }
+      nq += __popc(bal);
+      if (nq >= 32) {
+        __syncwarp();
+        part += bulk5_round(R, c, sm.queue, head, 32);
+        __syncwarp();
+        head = (head + 32) & 63;
+        nq -= 32;
+      }
+    }
+#else
     const uint32_t hl = ((uint32_t)h << 10) | (uint32_t)lane;
     uint32_t im = ch;
     while (im) {
@@ -858,6 +885,7 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
         nq -= 32;
       }
     }
+#endif
     // a bulk5 child is a whole (k-4)-node: poll every WM_BULK5_POLL_EVERY
     // children (the pipelined loads keep it cheap; every child over-donates)
     if (pollable && ++tc.poll >= WM_BULK5_POLL_EVERY) {
