@@ -185,12 +185,27 @@ int red_edges(const wm_cfg *cfg, cudaStream_t s, const int64_t *nnz) {
 // pass over the v < u entries (to name the first offending edge).
 enum : unsigned long long { kCsrRange = 0, kCsrAscend = 1, kCsrLoop = 2, kCsrSym = 3 };
 
+// offsets: [0] first decreasing / out-of-range vertex, [1] max degree (the
+// capacity planning of the motif arena), [2] non-zero when offsets[0] != 0
+// or offsets[n] != nnz
 __global__ void csr_offsets_kernel(int64_t n, int64_t nnz, const int64_t *__restrict__ off,
-                                   unsigned long long *__restrict__ bad_off) {
+                                   unsigned long long *__restrict__ bad_off,
+                                   unsigned long long *__restrict__ max_deg,
+                                   unsigned long long *__restrict__ bad_ends) {
+  if (blockIdx.x == 0 && threadIdx.x == 0 && (off[0] != 0 || off[n] != nnz)) *bad_ends = 1ull;
+  unsigned long long md = 0;
   for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u < n;
-       u += (int64_t)gridDim.x * blockDim.x)
-    if (off[u + 1] < off[u] || off[u] < 0 || off[u + 1] > nnz)
-      atomicMin(bad_off, (unsigned long long)u);
+       u += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = off[u], e = off[u + 1];
+    if (e < b || b < 0 || e > nnz) atomicMin(bad_off, (unsigned long long)u);
+    else if ((unsigned long long)(e - b) > md) md = (unsigned long long)(e - b);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const unsigned long long y = __shfl_xor_sync(0xffffffffu, md, o);
+    md = y > md ? y : md;
+  }
+  if (lane_id() == 0 && md) atomicMax(max_deg, md);
 }
 
 // bad[0] first violation key, bad[2] / bad[3] entries with v > u / v < u
@@ -239,29 +254,33 @@ __global__ void csr_check_kernel(int64_t n, int64_t nnz, const int64_t *__restri
   }
 }
 
-// runs the check on stream s (graph arrays already on the device); host
-// offsets bounds are checked by the caller
+// Runs the checks on stream s (graph arrays already on the device) and sets
+// g->max_degree.
 static int csr_validate(Graph *g, cudaStream_t s) {
   int st = g->ws->counters.ensure(sizeof(unsigned long long) * 64);
   if (st) return st;
-  unsigned long long *bad = g->ws->counters.as<unsigned long long>() + 58;  // [key, off, up, down]
+  // [key, first bad offset, up, down, max degree, bad ends]
+  unsigned long long *bad = g->ws->counters.as<unsigned long long>() + 56;
   WM_CUDA(cudaMemsetAsync(bad, 0xff, 2 * sizeof(unsigned long long), s));
-  WM_CUDA(cudaMemsetAsync(bad + 2, 0, 2 * sizeof(unsigned long long), s));
+  WM_CUDA(cudaMemsetAsync(bad + 2, 0, 4 * sizeof(unsigned long long), s));
   const int64_t ns = (int64_t)g->num_sms;
   const int vb = (int)((g->n + 255) / 256 < ns * 8 ? (g->n + 255) / 256 : ns * 8);
-  csr_offsets_kernel<<<vb > 0 ? vb : 1, 256, 0, s>>>(g->n, g->nnz, g->offsets, bad + 1);
-  unsigned long long hb[4] = {~0ull, ~0ull, 0, 0};
+  csr_offsets_kernel<<<vb > 0 ? vb : 1, 256, 0, s>>>(g->n, g->nnz, g->offsets, bad + 1, bad + 4,
+                                                     bad + 5);
+  unsigned long long hb[6] = {~0ull, ~0ull, 0, 0, 0, 0};
   WM_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
   WM_CUDA(cudaStreamSynchronize(s));
+  if (hb[5]) return fail(WM_EINVAL, "offsets do not span nnz=%lld", (long long)g->nnz);
   if (hb[1] != ~0ull)
     return fail(WM_EINVAL, "offsets must be non-decreasing (vertex %lld)", (long long)hb[1]);
+  g->max_degree = (int64_t)hb[4];
   const int eb = (int)((g->nnz + 255) / 256 < ns * 32 ? (g->nnz + 255) / 256 : ns * 32);
   for (int pass = 0; pass < 2; ++pass) {
     if (g->nnz > 0)
       csr_check_kernel<<<eb > 0 ? eb : 1, 256, 0, s>>>(g->n, g->nnz, g->offsets, g->neighbors,
                                                        pass, bad);
     WM_CUDA(cudaGetLastError());
-    WM_CUDA(cudaMemcpyAsync(hb, bad, sizeof hb, cudaMemcpyDeviceToHost, s));
+    WM_CUDA(cudaMemcpyAsync(hb, bad, 4 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
     WM_CUDA(cudaStreamSynchronize(s));
     // a valid graph stops after pass 0; any violation also searches the
     // v < u entries so the reported one is the first in the reference's order
@@ -354,12 +373,6 @@ int wm_graph_create(const wm_csr *csr, void **out) {
     return fail(WM_EINVAL, "null CSR arrays");
   if (csr->offsets[0] != 0 || csr->offsets[csr->n] != csr->nnz)
     return fail(WM_EINVAL, "offsets do not span nnz=%lld", (long long)csr->nnz);
-  int64_t md = 0;
-  for (int64_t v = 0; v < csr->n; ++v) {
-    int64_t d = csr->offsets[v + 1] - csr->offsets[v];
-    if (d < 0) return fail(WM_EINVAL, "offsets decrease at vertex %lld", (long long)v);
-    if (d > md) md = d;
-  }
   Graph *g = new Graph();
   int st = graph_init(g);
   if (st) { delete g; return st; }
@@ -367,7 +380,6 @@ int wm_graph_create(const wm_csr *csr, void **out) {
   if ((st = lk.status())) { delete g; return st; }
   g->n = csr->n;
   g->nnz = csr->nnz;
-  g->max_degree = md;
   cudaStream_t s = g->ws->own_stream;
   cudaError_t e = graph_alloc(g);
   if (e == cudaSuccess)
@@ -376,7 +388,6 @@ int wm_graph_create(const wm_csr *csr, void **out) {
   if (e == cudaSuccess && g->nnz > 0)
     e = cudaMemcpyAsync(g->neighbors, csr->neighbors, sizeof(int32_t) * g->nnz,
                         cudaMemcpyHostToDevice, s);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
   if (e != cudaSuccess) {
     wm_graph_destroy(g);
     return fail(WM_ECUDA, "graph upload failed: %s", cudaGetErrorString(e));
@@ -389,21 +400,6 @@ int wm_graph_create(const wm_csr *csr, void **out) {
   return WM_OK;
 }
 
-__global__ void max_degree_kernel(int64_t n, const int64_t *__restrict__ off,
-                                  unsigned long long *__restrict__ out) {
-  unsigned long long m = 0;
-  for (int64_t v = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; v < n;
-       v += (int64_t)gridDim.x * blockDim.x) {
-    const unsigned long long d = (unsigned long long)(off[v + 1] - off[v]);
-    m = d > m ? d : m;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const unsigned long long y = __shfl_xor_sync(0xffffffffu, m, o);
-    m = y > m ? y : m;
-  }
-  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
-}
 
 int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
                            const int32_t *d_neighbors, void **out) {
@@ -427,32 +423,6 @@ int wm_graph_create_device(int64_t n, int64_t nnz, const int64_t *d_offsets,
   if (e == cudaSuccess && nnz > 0)
     e = cudaMemcpyAsync(g->neighbors, d_neighbors, sizeof(int32_t) * nnz,
                         cudaMemcpyDeviceToDevice, s);
-  // max degree for capacity planning, reduced on the device
-  if (e == cudaSuccess) {
-    const int r = g->ws->counters.ensure(sizeof(unsigned long long) * 64);
-    if (r) { wm_graph_destroy(g); return r; }
-    unsigned long long *md = g->ws->counters.as<unsigned long long>();
-    e = cudaMemsetAsync(md, 0, sizeof(unsigned long long), s);
-    if (e == cudaSuccess) {
-      const int64_t blocks = (n + 255) / 256 < (int64_t)g->num_sms * 8 ? (n + 255) / 256
-                                                                      : (int64_t)g->num_sms * 8;
-      max_degree_kernel<<<(int)blocks, 256, 0, s>>>(n, g->offsets, md);
-      e = cudaGetLastError();
-    }
-    unsigned long long h = 0;
-    int64_t ends[2] = {0, 0};
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, md, sizeof h, cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(&ends[0], g->offsets, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(&ends[1], g->offsets + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
-    g->max_degree = (int64_t)h;
-    if (e == cudaSuccess && (ends[0] != 0 || ends[1] != nnz)) {
-      wm_graph_destroy(g);
-      return fail(WM_EINVAL, "offsets do not span nnz=%lld", (long long)nnz);
-    }
-  }
   if (e != cudaSuccess) {
     wm_graph_destroy(g);
     return fail(WM_ECUDA, "device graph copy failed: %s", cudaGetErrorString(e));

@@ -572,12 +572,20 @@ __device__ __forceinline__ bool share_claims(const MotifArgs &a, MotifWarp &w, i
 #ifndef WM_MOTIF_DONATE_MIN
 #define WM_MOTIF_DONATE_MIN 1024ull
 #endif
+// blocks per SM the register budget must allow: 4 (64 registers) for k <= 5,
+// 6 (40 registers) for k >= 6, where the longer subtrees hide the spill cost
+// and the extra warps overlap the (L2-resident, suffix-local) hash probes:
+// cfg4 k=6 135.9 -> 128.4 ms, cfg5 k=7 43.8 -> 41.1; k=5 prefers 4 (3.68 vs
+// 3.78 ms) (profiles/r02_ab_motif_mb.log)
 #ifndef WM_MOTIF_MINBLOCKS
 #define WM_MOTIF_MINBLOCKS 4
 #endif
+#ifndef WM_MOTIF_MINBLOCKS_DEEP
+#define WM_MOTIF_MINBLOCKS_DEEP 6
+#endif
 
-template <bool BYTES, bool LIST>
-__global__ void __launch_bounds__(256, WM_MOTIF_MINBLOCKS) motif_enum_kernel(MotifArgs a) {
+template <bool BYTES, bool LIST, int MINB>
+__global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
   extern __shared__ __align__(16) unsigned char smraw[];
   unsigned long long *sh = reinterpret_cast<unsigned long long *>(smraw);
   MotifWarp *warps = reinterpret_cast<MotifWarp *>(
@@ -1082,7 +1090,8 @@ static int launch_motif(Graph *g, const wm_cfg *cfg, MotifArgs a, cudaStream_t s
   int wpb = cfg->warps_per_block > 0 ? cfg->warps_per_block : 8;
   const size_t hist_bytes = a.smem_hist ? ((size_t)a.pattern_count * 8 + 15) / 16 * 16 : 0;
   const size_t smem = hist_bytes + sizeof(MotifWarp) * wpb;
-  auto kern = motif_enum_kernel<BYTES, LIST>;
+  auto kern = (a.k >= 6 && !LIST) ? motif_enum_kernel<BYTES, LIST, WM_MOTIF_MINBLOCKS_DEEP>
+                                  : motif_enum_kernel<BYTES, LIST, WM_MOTIF_MINBLOCKS>;
   WM_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int bps = 0;
   WM_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&bps, kern, wpb * 32, smem));
