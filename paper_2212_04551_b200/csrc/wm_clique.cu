@@ -203,6 +203,10 @@ template <int W> struct BuildSmem {
   uint32_t adj[D * W];
   int32_t pre[D + 1];
   int64_t rowbeg[D];
+#if WM_BUILD_HASH
+  int32_t hkey[2 * D];        // member id -> local index, open addressing (load <= 1/2)
+  int32_t hval[2 * D];
+#endif
 };
 
 template <int W>
@@ -274,6 +278,37 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
     }
     __syncwarp();
     const int total = carry;
+#if WM_BUILD_HASH
+    // members into a small hash table (member id -> local index): one or two
+    // shared loads per membership test instead of a log2(d) binary search;
+    // each lane walks the flattened (row, element) pairs with a row cursor
+    // that only moves forward instead of searching the row per element
+    int tb = 5;
+    while ((1 << tb) < 2 * d) ++tb;
+    const int T = 1 << tb;
+    for (int i = lane; i < T; i += 32) sm.hkey[i] = -1;
+    __syncwarp();
+    for (int i = lane; i < d; i += 32) {
+      const int32_t x = sm.list[i];
+      uint32_t h = ((uint32_t)x * 0x9E3779B1u) >> (32 - tb);
+      while (atomicCAS(&sm.hkey[h], -1, x) != -1) h = (h + 1) & (uint32_t)(T - 1);
+      sm.hval[h] = sm.rk[i];
+    }
+    __syncwarp();
+    int r = 0;
+#pragma unroll 2
+    for (int f = lane; f < total; f += 32) {
+      while (r + 1 < d && sm.pre[r + 1] <= f) ++r;
+      const int32_t x = __ldg(dnbr + sm.rowbeg[r] + (f - sm.pre[r]));
+      uint32_t h = ((uint32_t)x * 0x9E3779B1u) >> (32 - tb);
+      int32_t kx;
+      while ((kx = sm.hkey[h]) != x && kx != -1) h = (h + 1) & (uint32_t)(T - 1);
+      if (kx == x) {
+        const int b = sm.hval[h];
+        atomicOr(&sm.adj[sm.rk[r] * wv + (b >> 5)], 1u << (b & 31));
+      }
+    }
+#else
     // flattened (row, element) pairs: every lane busy regardless of row length
     for (int f0 = 0; f0 < total; f0 += 128) {
       int32_t xs[4];
@@ -303,6 +338,7 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
         }
       }
     }
+#endif
     __syncwarp();
     uint32_t *out = bm + bm_off[t];
     for (int i = lane; i < d * wv; i += 32) out[i] = sm.adj[i];

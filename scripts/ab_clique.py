@@ -12,12 +12,15 @@ if len(sys.argv) > 2 and sys.argv[1] == "--one":
     k = int(sys.argv[2])
     g = synth.config_graph(os.environ.get("WM_AB_CFG", "cfg3"))
     bc = BalanceConfig(threshold=1.0, poll_interval=int(os.environ.get("WM_POLL", "32")))
-    ms = []
+    ms, bms, dms = [], [], []
     for i in range(int(os.environ.get("WM_AB_REPS", "6"))):
         r = run_clique(g, k, mode="opt", balance_config=bc)
         if i:
             ms.append(r.kernel_ms)
+            bms.append(r.extra["build_ms"])
+            dms.append(r.device_ms)
     print(json.dumps({"k": k, "kernel_ms": statistics.median(ms), "min": min(ms),
+                      "build_ms": statistics.median(bms), "device_ms": statistics.median(dms),
                       "count": r.clique_count, "warps": r.warps,
                       "idle": round(r.idle_warp_fraction, 3), "migr": r.migrations}))
     sys.exit(0)
