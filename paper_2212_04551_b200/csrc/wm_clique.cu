@@ -203,7 +203,10 @@ template <int W> struct BuildSmem {
   uint32_t adj[D * W];
   int32_t pre[D + 1];
   int64_t rowbeg[D];
-#if WM_BUILD_HASH
+#ifndef WM_BUILD_BATCH
+#define WM_BUILD_BATCH 8
+#endif
+#ifndef WM_BUILD_BSEARCH
   int32_t hkey[2 * D];        // member id -> local index, open addressing (load <= 1/2)
   int32_t hval[2 * D];
 #endif
@@ -278,11 +281,14 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
     }
     __syncwarp();
     const int total = carry;
-#if WM_BUILD_HASH
+#ifndef WM_BUILD_BSEARCH
     // members into a small hash table (member id -> local index): one or two
     // shared loads per membership test instead of a log2(d) binary search;
     // each lane walks the flattened (row, element) pairs with a row cursor
-    // that only moves forward instead of searching the row per element
+    // that only moves forward instead of searching the row per element, 8
+    // elements per batch so their loads are in flight together: cfg5 k=8
+    // build 30.7 -> 23.5 ms (profiles/r02_ab_bhash2.log; WM_BUILD_BSEARCH=1
+    // restores the binary searches)
     int tb = 5;
     while ((1 << tb) < 2 * d) ++tb;
     const int T = 1 << tb;
@@ -296,16 +302,31 @@ __global__ void __launch_bounds__(256) clique_build_kernel(const int64_t *__rest
     }
     __syncwarp();
     int r = 0;
-#pragma unroll 2
-    for (int f = lane; f < total; f += 32) {
-      while (r + 1 < d && sm.pre[r + 1] <= f) ++r;
-      const int32_t x = __ldg(dnbr + sm.rowbeg[r] + (f - sm.pre[r]));
-      uint32_t h = ((uint32_t)x * 0x9E3779B1u) >> (32 - tb);
-      int32_t kx;
-      while ((kx = sm.hkey[h]) != x && kx != -1) h = (h + 1) & (uint32_t)(T - 1);
-      if (kx == x) {
-        const int b = sm.hval[h];
-        atomicOr(&sm.adj[sm.rk[r] * wv + (b >> 5)], 1u << (b & 31));
+    for (int f0 = lane; f0 < total; f0 += 32 * WM_BUILD_BATCH) {
+      // the batch's rows (cursor moves forward), then all its loads in flight
+      int rows[WM_BUILD_BATCH];
+      int32_t xs[WM_BUILD_BATCH];
+#pragma unroll
+      for (int j = 0; j < WM_BUILD_BATCH; ++j) {
+        const int f = f0 + 32 * j;
+        rows[j] = -1;
+        if (f < total) {
+          while (r + 1 < d && sm.pre[r + 1] <= f) ++r;
+          rows[j] = r;
+          xs[j] = __ldg(dnbr + sm.rowbeg[r] + (f - sm.pre[r]));
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < WM_BUILD_BATCH; ++j) {
+        if (rows[j] < 0) continue;
+        const int32_t x = xs[j];
+        uint32_t h = ((uint32_t)x * 0x9E3779B1u) >> (32 - tb);
+        int32_t kx;
+        while ((kx = sm.hkey[h]) != x && kx != -1) h = (h + 1) & (uint32_t)(T - 1);
+        if (kx == x) {
+          const int b = sm.hval[h];
+          atomicOr(&sm.adj[sm.rk[rows[j]] * wv + (b >> 5)], 1u << (b & 31));
+        }
       }
     }
 #else
