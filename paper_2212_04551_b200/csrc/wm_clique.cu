@@ -384,6 +384,9 @@ template <int WMAX> struct alignas(16) CliqueSmem {  // 16B: uint4 row loads
   unsigned long long below[kMaxK];     // leaves under the level's node (B_alg)
   int32_t last[kMaxK];                 // vertex appended at the level
   uint32_t queue[96];                  // bulk4/5 ring (64) + a scratch slot per lane
+#ifndef WM_BULK5_CHILDPUSH
+  uint32_t pq[64];                     // bulk5 (h, i) pair ring
+#endif
   uint32_t crow[32];                   // bulk4 node compacted to <= 32 members
 };
 
@@ -897,6 +900,87 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
   const bool pollable = a.lb_on && __popc(pc) >= WM_BULK5_POLL_MIN;
   unsigned long long part = 0;
   int head = 0, nq = 0;
+#ifndef WM_BULK5_CHILDPUSH
+  // (h, i) pairs of several children flattened through a 64-entry pair ring,
+  // 32 per batch (one per lane, word = C_hi): push rounds then run with most
+  // lanes busy instead of |C_h| of them (a child has few members: the
+  // per-child rounds pushed ~4 triples each).  cfg3 k=8 5.85 -> 5.22 ms, k=9
+  // 26.46 -> 21.43, k=10 118.7 -> 93.3, cfg5 k=8 67.9 -> 53.5
+  // (profiles/r02_ab_pairq.log; WM_BULK5_CHILDPUSH=1 restores per-child rounds)
+  const uint32_t lt = (1u << lane) - 1u;
+  int phead = 0, pn = 0;
+  while (pc || pn) {
+    while (pc && pn < 32) {
+      const int h = pop_hi(pc);
+      const uint32_t ch = c & R[h];
+      if ((ch >> lane) & 1u) sm.pq[(phead + pn + __popc(ch & lt)) & 63] = ((uint32_t)h << 5) | lane;
+      pn += __popc(ch);
+      // a bulk5 child is a whole (k-4)-node: poll every WM_BULK5_POLL_EVERY
+      // children (the pipelined loads keep it cheap; every child over-donates)
+      if (pollable && ++tc.poll >= WM_BULK5_POLL_EVERY) {
+        tc.poll = 0;
+        ++tc.polls;
+        int want = 0;
+        if (lane == 0) {
+          want = (int)(pt - ph) >= a.idle_min;
+          pt = (uint32_t)ld_relaxed(&a.L.lb->tail);
+          ph = (uint32_t)ld_relaxed(&a.L.lb->head);
+        }
+        if (__shfl_sync(0xffffffffu, want, 0)) {
+          // expose the pending children in the original bit space, donate,
+          // take back what is left
+          if (w == 1) {
+            if (lane == 0) sm.P[lv] = pc;
+            __syncwarp();
+            try_donate<w>(sm.C, sm.P, a, s0, lv, task);
+            pc = sm.P[lv];
+          } else {
+            const bool mine = lane < m && ((pc >> lane) & 1u);
+#pragma unroll
+            for (int x = 0; x < w; ++x) {
+              const uint32_t v =
+                  __reduce_or_sync(0xffffffffu, (mine && (pos >> 5) == x) ? 1u << (pos & 31) : 0u);
+              if (lane == 0) sm.P[lv * w + x] = v;
+            }
+            __syncwarp();
+            try_donate<w>(sm.C, sm.P, a, s0, lv, task);
+            pc = __ballot_sync(0xffffffffu,
+                               lane < m && ((sm.P[lv * w + (pos >> 5)] >> (pos & 31)) & 1u));
+          }
+          __syncwarp();
+        }
+      }
+    }
+    __syncwarp();
+    const int take = pn < 32 ? pn : 32;
+    uint32_t word = 0u, hi5 = 0u;
+    if (lane < take) {
+      const uint32_t e = sm.pq[(phead + lane) & 63];
+      const int h = (int)(e >> 5), i = (int)(e & 31u);
+      word = c & R[h] & R[i];
+      hi5 = ((uint32_t)h << 10) | ((uint32_t)i << 5);
+    }
+    phead = (phead + take) & 63;
+    pn -= take;
+    __syncwarp();
+    for (;;) {
+      const unsigned bal = __ballot_sync(0xffffffffu, word != 0u);
+      if (!bal) break;
+      if (word) {
+        const int j = pop_hi(word);
+        sm.queue[(head + nq + __popc(bal & lt)) & 63] = hi5 | (uint32_t)j;
+      }
+      nq += __popc(bal);
+      if (nq >= 32) {
+        __syncwarp();
+        part += bulk5_round(R, c, sm.queue, head, 32);
+        __syncwarp();
+        head = (head + 32) & 63;
+        nq -= 32;
+      }
+    }
+  }
+#else
   while (pc) {
     const int h = pop_hi(pc);
     const uint32_t ch = c & R[h];
@@ -979,6 +1063,7 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
       }
     }
   }
+#endif
   if (nq) {
     __syncwarp();
     part += bulk5_round(R, c, sm.queue, head, nq);
