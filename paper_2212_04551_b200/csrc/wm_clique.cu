@@ -384,9 +384,7 @@ template <int WMAX> struct alignas(16) CliqueSmem {  // 16B: uint4 row loads
   unsigned long long below[kMaxK];     // leaves under the level's node (B_alg)
   int32_t last[kMaxK];                 // vertex appended at the level
   uint32_t queue[96];                  // bulk4/5 ring (64) + a scratch slot per lane
-#ifndef WM_BULK5_CHILDPUSH
   uint32_t pq[64];                     // bulk5 (h, i) pair ring
-#endif
   uint32_t crow[32];                   // bulk4 node compacted to <= 32 members
 };
 
@@ -839,15 +837,15 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
 // (compaction, child pops, partial rounds) disappears: the bulk4 node of each
 // child h is just the word C_h = c & R[h].  Returns false (nothing done) when
 // the node is too wide to compact; the DFS then continues to bulk4.
-__device__ __forceinline__ unsigned long long bulk5_round(const uint32_t *R, uint32_t c,
+// One round: each lane takes one queued candidate set C_hij (its (h, i, j)
+// triple's set, computed at push time) and counts the edges inside it.
+__device__ __forceinline__ unsigned long long bulk5_round(const uint32_t *R,
                                                           const uint32_t *queue, int head,
                                                           int nq) {
   const int lane = lane_id();
   uint32_t part = 0;  // <= 32 * 32 per round
   if (lane < nq) {
-    const uint32_t e = queue[(head + lane) & 63];
-    const int h = (int)(e >> 10), i = (int)((e >> 5) & 31u), j = (int)(e & 31u);
-    const uint32_t cij = c & R[h] & R[i] & R[j];
+    const uint32_t cij = queue[(head + lane) & 63];
     uint32_t m = cij;
     m &= m - 1u;  // rows are lower-triangular: the lowest member adds nothing
     while (m) part += __popc(cij & R[pop_hi(m)]);
@@ -900,13 +898,14 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
   const bool pollable = a.lb_on && __popc(pc) >= WM_BULK5_POLL_MIN;
   unsigned long long part = 0;
   int head = 0, nq = 0;
-#ifndef WM_BULK5_CHILDPUSH
   // (h, i) pairs of several children flattened through a 64-entry pair ring,
   // 32 per batch (one per lane, word = C_hi): push rounds then run with most
   // lanes busy instead of |C_h| of them (a child has few members: the
   // per-child rounds pushed ~4 triples each).  cfg3 k=8 5.85 -> 5.22 ms, k=9
   // 26.46 -> 21.43, k=10 118.7 -> 93.3, cfg5 k=8 67.9 -> 53.5
-  // (profiles/r02_ab_pairq.log; WM_BULK5_CHILDPUSH=1 restores per-child rounds)
+  // (profiles/r02_ab_pairq.log).  The ring holds the triples' candidate sets
+  // C_hij themselves (computed at push), and sets with < 2 members — no edge,
+  // nothing to count — are not queued at all.
   const uint32_t lt = (1u << lane) - 1u;
   int phead = 0, pn = 0;
   while (pc || pn) {
@@ -953,120 +952,37 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
     }
     __syncwarp();
     const int take = pn < 32 ? pn : 32;
-    uint32_t word = 0u, hi5 = 0u;
+    uint32_t ci = 0u;
     if (lane < take) {
       const uint32_t e = sm.pq[(phead + lane) & 63];
-      const int h = (int)(e >> 5), i = (int)(e & 31u);
-      word = c & R[h] & R[i];
-      hi5 = ((uint32_t)h << 10) | ((uint32_t)i << 5);
+      ci = c & R[e >> 5] & R[e & 31u];  // C_hi
     }
     phead = (phead + take) & 63;
     pn -= take;
     __syncwarp();
+    // each j of C_hi: C_hij = C_hi & R[j] goes into the ring unless it has
+    // fewer than two members (no edge inside: nothing to count)
+    uint32_t word = ci;
     for (;;) {
-      const unsigned bal = __ballot_sync(0xffffffffu, word != 0u);
-      if (!bal) break;
-      if (word) {
-        const int j = pop_hi(word);
-        sm.queue[(head + nq + __popc(bal & lt)) & 63] = hi5 | (uint32_t)j;
-      }
+      if (!__any_sync(0xffffffffu, word != 0u)) break;
+      uint32_t t = 0u;
+      if (word) t = ci & R[pop_hi(word)];
+      const bool keep = (t & (t - 1u)) != 0u;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) sm.queue[(head + nq + __popc(bal & lt)) & 63] = t;
       nq += __popc(bal);
       if (nq >= 32) {
         __syncwarp();
-        part += bulk5_round(R, c, sm.queue, head, 32);
+        part += bulk5_round(R, sm.queue, head, 32);
         __syncwarp();
         head = (head + 32) & 63;
         nq -= 32;
       }
     }
   }
-#else
-  while (pc) {
-    const int h = pop_hi(pc);
-    const uint32_t ch = c & R[h];
-#ifndef WM_BULK5_WARPPUSH
-    // members are bit positions < 32, so lane i owns member i of ch: all the
-    // (h, i) pairs of the child at once, word_i = C_hi; each round every lane
-    // with j's left pushes one triple (ballot-compacted into the ring), so a
-    // child costs max_i |C_hi| rounds instead of one warp-wide trip per i
-    // (k=9 26.68 -> 26.46 ms, k=10 120.5 -> 118.6; profiles/r02_ab_lanepush.log;
-    // WM_BULK5_WARPPUSH=1 restores the per-i form)
-    uint32_t word = ((ch >> lane) & 1u) ? (ch & R[lane]) : 0u;
-    const uint32_t hi5 = ((uint32_t)h << 10) | ((uint32_t)lane << 5);
-    const uint32_t lt = (1u << lane) - 1u;
-    for (;;) {
-      const unsigned bal = __ballot_sync(0xffffffffu, word != 0u);
-      if (!bal) break;
-      if (word) {
-        const int j = pop_hi(word);
-        sm.queue[(head + nq + __popc(bal & lt)) & 63] = hi5 | (uint32_t)j;
-      }
-      nq += __popc(bal);
-      if (nq >= 32) {
-        __syncwarp();
-        part += bulk5_round(R, c, sm.queue, head, 32);
-        __syncwarp();
-        head = (head + 32) & 63;
-        nq -= 32;
-      }
-    }
-#else
-    const uint32_t hl = ((uint32_t)h << 10) | (uint32_t)lane;
-    uint32_t im = ch;
-    while (im) {
-      const int i = pop_hi(im);
-      const uint32_t word = ch & R[i];
-      sm.queue[ring_slot(word, head + nq)] = hl | ((uint32_t)i << 5);
-      nq += __popc(word);
-      if (nq >= 32) {
-        __syncwarp();
-        part += bulk5_round(R, c, sm.queue, head, 32);
-        __syncwarp();
-        head = (head + 32) & 63;
-        nq -= 32;
-      }
-    }
-#endif
-    // a bulk5 child is a whole (k-4)-node: poll every WM_BULK5_POLL_EVERY
-    // children (the pipelined loads keep it cheap; every child over-donates)
-    if (pollable && ++tc.poll >= WM_BULK5_POLL_EVERY) {
-      tc.poll = 0;
-      ++tc.polls;
-      int want = 0;
-      if (lane == 0) {
-        want = (int)(pt - ph) >= a.idle_min;
-        pt = (uint32_t)ld_relaxed(&a.L.lb->tail);
-        ph = (uint32_t)ld_relaxed(&a.L.lb->head);
-      }
-      if (__shfl_sync(0xffffffffu, want, 0)) {
-        // expose the pending children in the original bit space, donate,
-        // take back what is left
-        if (w == 1) {
-          if (lane == 0) sm.P[lv] = pc;
-          __syncwarp();
-          try_donate<w>(sm.C, sm.P, a, s0, lv, task);
-          pc = sm.P[lv];
-        } else {
-          const bool mine = lane < m && ((pc >> lane) & 1u);
-#pragma unroll
-          for (int x = 0; x < w; ++x) {
-            const uint32_t v =
-                __reduce_or_sync(0xffffffffu, (mine && (pos >> 5) == x) ? 1u << (pos & 31) : 0u);
-            if (lane == 0) sm.P[lv * w + x] = v;
-          }
-          __syncwarp();
-          try_donate<w>(sm.C, sm.P, a, s0, lv, task);
-          pc = __ballot_sync(0xffffffffu,
-                             lane < m && ((sm.P[lv * w + (pos >> 5)] >> (pos & 31)) & 1u));
-        }
-        __syncwarp();
-      }
-    }
-  }
-#endif
   if (nq) {
     __syncwarp();
-    part += bulk5_round(R, c, sm.queue, head, nq);
+    part += bulk5_round(R, sm.queue, head, nq);
     __syncwarp();
   }
   out = part;
