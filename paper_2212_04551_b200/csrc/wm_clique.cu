@@ -903,17 +903,23 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
   // lanes busy instead of |C_h| of them (a child has few members: the
   // per-child rounds pushed ~4 triples each).  cfg3 k=8 5.85 -> 5.22 ms, k=9
   // 26.46 -> 21.43, k=10 118.7 -> 93.3, cfg5 k=8 67.9 -> 53.5
-  // (profiles/r02_ab_pairq.log).  The ring holds the triples' candidate sets
-  // C_hij themselves (computed at push), and sets with < 2 members — no edge,
-  // nothing to count — are not queued at all.
+  // (profiles/r02_ab_pairq.log).  The rings hold the candidate sets themselves
+  // (C_hi, C_hij, computed at push) and skip every set too small to reach a
+  // counted edge (child < 4, pair < 3, triple < 2 members): k=9 21.4 -> 19.0
+  // ms, k=10 93.2 -> 81.8 (profiles/r02_ab_cijq.log, r02_ab_cijq2.log).
   const uint32_t lt = (1u << lane) - 1u;
   int phead = 0, pn = 0;
   while (pc || pn) {
     while (pc && pn < 32) {
       const int h = pop_hi(pc);
       const uint32_t ch = c & R[h];
-      if ((ch >> lane) & 1u) sm.pq[(phead + pn + __popc(ch & lt)) & 63] = ((uint32_t)h << 5) | lane;
-      pn += __popc(ch);
+      // a child needs >= 4 candidates and a pair >= 3 to reach a counted edge:
+      // queue C_hi itself for the pairs that can
+      const uint32_t ci = ((ch >> lane) & 1u) ? (ch & R[lane]) : 0u;
+      const bool pk = __popc(ch) >= 4 && __popc(ci) >= 3;
+      const unsigned pb = __ballot_sync(0xffffffffu, pk);
+      if (pk) sm.pq[(phead + pn + __popc(pb & lt)) & 63] = ci;
+      pn += __popc(pb);
       // a bulk5 child is a whole (k-4)-node: poll every WM_BULK5_POLL_EVERY
       // children (the pipelined loads keep it cheap; every child over-donates)
       if (pollable && ++tc.poll >= WM_BULK5_POLL_EVERY) {
@@ -952,11 +958,7 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
     }
     __syncwarp();
     const int take = pn < 32 ? pn : 32;
-    uint32_t ci = 0u;
-    if (lane < take) {
-      const uint32_t e = sm.pq[(phead + lane) & 63];
-      ci = c & R[e >> 5] & R[e & 31u];  // C_hi
-    }
+    const uint32_t ci = lane < take ? sm.pq[(phead + lane) & 63] : 0u;  // C_hi
     phead = (phead + take) & 63;
     pn -= take;
     __syncwarp();
