@@ -503,6 +503,7 @@ def main():
             "migrations": ro.migrations, "donations": ro.rebalance_count}
         extras["secondary"] = secondary_workloads(stream)
         extras["cfg3_other_k"] = other_k(args, g, gold, stream, flush, bc)
+        extras["cfg5_clique_k12"] = cfg5_k12(gold, stream, flush, bc)
     if world == 1 and not args.no_motif:
         extras["motif"] = motif_block(args, stream, flush, gold, peak, peak_src, ncu)
     cpu = None
@@ -665,6 +666,26 @@ def other_k(args, g, gold, stream, flush, bc):
                           "count_matches_golden": want is None or
                           all(r.clique_count == want for r in rs)}
     return out
+
+
+def cfg5_k12(gold, stream, flush, bc):
+    """BASELINE config 5's clique workload: 12-cliques of the R-MAT scale-22
+    graph (2.2e11 of them), one warm-up and two timed steps (~4 s each),
+    checked against the pinned count; ``shard_scaling.py`` has its 8-shard
+    balance."""
+    from paper_2212_04551_b200 import run_clique, synth
+    g5 = synth.config_graph("cfg5")
+    want = gold.get("cfg5", {}).get("clique", {}).get("12", {}).get("count")
+    run_clique(g5, 12, mode="opt", balance_config=bc, stream=stream)
+    ms, rs, clk = timed_steps(lambda: run_clique(g5, 12, mode="opt", balance_config=bc,
+                                                 stream=stream), 2, stream, flush, 1)
+    return {"workload": "cfg5 12-clique counting, R-MAT scale 22 (n=%d, m=%d)" % (g5.n, g5.m),
+            "value": sum(r.clique_count for r in rs) / (sum(ms) * 1e-3), "unit": UNIT,
+            "ms_per_step": sum(ms) / len(ms),
+            "kernel_ms": statistics.mean(r.kernel_ms for r in rs),
+            "count_per_step": rs[0].clique_count,
+            "count_matches_golden": want is None or all(r.clique_count == want for r in rs),
+            "idle_warp_fraction": rs[0].idle_warp_fraction, "clocks": clk}
 
 
 def secondary_workloads(stream):
