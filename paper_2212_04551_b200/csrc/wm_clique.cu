@@ -1609,6 +1609,11 @@ struct CliqueIndex {
   unsigned long long arena_words = 0;
   std::vector<int32_t> sorted_deg;     // host: out-degree of tasks[i] (descending)
   std::vector<std::vector<int32_t>> wide;  // host: members of the roots with d > 1024
+  // Union graph of the roots with 128 < d <= 1024 (clique_union_get): the
+  // disjoint union of their out-neighbourhoods' induced subgraphs; its
+  // (k-1)-cliques are exactly the k-cliques rooted at those roots.
+  Graph *ug = nullptr;
+  bool union_tried = false;
 };
 
 void clique_index_free(Graph *g) {
@@ -1621,9 +1626,70 @@ void clique_index_free(Graph *g) {
       cudaFreeAsync(ix->dag_nbr, s);
       cudaFreeAsync(ix->tasks, s);
       cudaFreeAsync(ix->bm_off, s);
+      if (ix->ug) {
+        cudaFreeAsync(ix->ug->offsets, s);
+        cudaFreeAsync(ix->ug->neighbors, s);
+      }
+    }
+    if (ix->ug) {
+      clique_index_free(ix->ug);
+      delete ix->ug;
     }
     delete ix;
     g->cidx[o] = nullptr;
+  }
+}
+
+// Union-graph rows of one wide-class root per warp: local member i's row is
+// A[i] | A^T[i] over the root's bitmap (A lower-triangular: members ranked
+// above i; the transpose adds those ranked below), i.e. i's neighbours inside
+// the root's out-neighbourhood, emitted in ascending local index = ascending
+// union id (moff[r] + local).  Pass 1 (out == nullptr) writes the degrees.
+__global__ void union_rows_kernel(const int32_t *__restrict__ tasks,
+                                  const int64_t *__restrict__ doff,
+                                  const unsigned long long *__restrict__ bm_off,
+                                  const uint32_t *__restrict__ bm, unsigned long long first,
+                                  unsigned long long cnt, const int64_t *__restrict__ moff,
+                                  int64_t *__restrict__ udeg, const int64_t *__restrict__ uoff,
+                                  int32_t *__restrict__ out) {
+  const int lane = lane_id();
+  const unsigned long long nw = ((unsigned long long)gridDim.x * blockDim.x) >> 5;
+  for (unsigned long long r = ((unsigned long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+       r < cnt; r += nw) {
+    const unsigned long long t = first + r;
+    const int32_t v = __ldg(tasks + t);
+    const int d = (int)(__ldg(doff + v + 1) - __ldg(doff + v));
+    const int wv = (d + 31) >> 5;
+    const uint32_t *A = bm + __ldg(bm_off + t);
+    const int64_t base = __ldg(moff + r);
+    for (int i = 0; i < d; ++i) {
+      uint32_t mine = 0u;  // lane x < wv: word x of row i of A | A^T
+      for (int x = 0; x < wv; ++x) {
+        const int j = 32 * x + lane;
+        const bool tb = j < d && ((__ldg(A + (size_t)j * wv + (i >> 5)) >> (i & 31)) & 1u);
+        const uint32_t tw = __ballot_sync(0xffffffffu, tb);
+        if (lane == x) mine = __ldg(A + (size_t)i * wv + x) | tw;
+      }
+      const int c = __popc(mine);
+      if (!out) {
+        const int deg = __reduce_add_sync(0xffffffffu, c);
+        if (lane == 0) udeg[base + i] = deg;
+      } else {
+        int pre = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int z = __shfl_up_sync(0xffffffffu, pre, o);
+          if (lane >= o) pre += z;
+        }
+        int64_t pos = uoff[base + i] + (pre - c);
+        uint32_t m = mine;
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1u;
+          out[pos++] = (int32_t)(base + 32 * lane + b);
+        }
+      }
+    }
   }
 }
 
@@ -1735,6 +1801,96 @@ static int clique_index_get(Graph *g, int order, cudaStream_t s, CliqueIndex **o
   return WM_OK;
 }
 
+// Builds (once per graph and orientation) the union graph of the roots whose
+// out-degree is in (128, 1024]: their bitmaps (the same per-root build as a
+// run) turned into the symmetric adjacency of each out-neighbourhood, one
+// disjoint component per root.  Such roots otherwise run in the W = 8..32
+// enumeration classes (106+ registers, 9+ KB of shared memory per warp: 16
+// warps per SM); the union's own tasks are narrow and run in the W <= 4 class
+// at 40 warps per SM.
+static int clique_union_get(Graph *g, CliqueIndex *ix, int order, cudaStream_t s) {
+  if (ix->ug || ix->union_tried) return WM_OK;
+  ix->union_tried = true;
+  const std::vector<int32_t> &sd = ix->sorted_deg;
+  unsigned long long nwide = 0, nunion = 0;
+  while (nwide < sd.size() && sd[nwide] > 1024) ++nwide;
+  while (nwide + nunion < sd.size() && sd[nwide + nunion] > 128) ++nunion;
+  if (!nunion) return WM_OK;
+  // member offsets (host; sorted degrees are cached)
+  std::vector<int64_t> moff(nunion + 1, 0);
+  for (unsigned long long r = 0; r < nunion; ++r) moff[r + 1] = moff[r] + sd[nwide + r];
+  const int64_t U = moff[nunion];
+  int st;
+  if ((st = g->ws->arena.ensure(sizeof(uint32_t) * (ix->arena_words + 1)))) return st;
+  // bitmaps of the union roots, bucket by bucket (c = 5, 4, 3: W = 32, 16, 8)
+  {
+    unsigned long long begin = nwide;
+    for (int c = 5; c >= 3; --c) {
+      unsigned long long cnt = 0;
+      while (begin + cnt < nwide + nunion && sd[begin + cnt] > (32 << (c - 1))) ++cnt;
+      if (!cnt) continue;
+      CliqueArgs a;
+      a.doff = ix->dag_off;
+      a.dnbr = ix->dag_nbr;
+      a.tasks = ix->tasks + begin;
+      a.bm_off = ix->bm_off + begin;
+      a.bm = g->ws->arena.as<uint32_t>();
+      switch (c) {
+        case 5: st = launch_build<32>(g, a, cnt, cnt, cnt, 1, order, 1, s); break;
+        case 4: st = launch_build<16>(g, a, cnt, cnt, cnt, 1, order, 1, s); break;
+        default: st = launch_build<8>(g, a, cnt, cnt, cnt, 1, order, 1, s); break;
+      }
+      if (st) return st;
+      begin += cnt;
+    }
+  }
+  int64_t *dmoff = nullptr, *udeg = nullptr, *uoff = nullptr;
+  void *tmp = nullptr;
+  size_t tb = 0;
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tb, udeg, uoff, (int)(U + 1), s));
+  WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&dmoff), sizeof(int64_t) * (nunion + 1),
+                                  g->ws->pool, s));
+  WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&udeg), sizeof(int64_t) * (U + 1),
+                                  g->ws->pool, s));
+  WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&uoff), sizeof(int64_t) * (U + 1),
+                                  g->ws->pool, s));
+  WM_CUDA(cudaMallocFromPoolAsync(&tmp, tb > 0 ? tb : 16, g->ws->pool, s));
+  WM_CUDA(cudaMemcpyAsync(dmoff, moff.data(), sizeof(int64_t) * (nunion + 1),
+                          cudaMemcpyHostToDevice, s));
+  WM_CUDA(cudaMemsetAsync(udeg + U, 0, sizeof(int64_t), s));
+  const int64_t want = ((int64_t)nunion * 32 + 255) / 256;
+  const int blocks = (int)(want < (int64_t)g->num_sms * 16 ? want : (int64_t)g->num_sms * 16);
+  union_rows_kernel<<<blocks, 256, 0, s>>>(ix->tasks, ix->dag_off, ix->bm_off,
+                                           g->ws->arena.as<uint32_t>(), nwide, nunion, dmoff,
+                                           udeg, nullptr, nullptr);
+  WM_CUDA(cudaGetLastError());
+  WM_CUDA(cub::DeviceScan::ExclusiveSum(tmp, tb, udeg, uoff, (int)(U + 1), s));
+  int64_t nnz = 0;
+  WM_CUDA(cudaMemcpyAsync(&nnz, uoff + U, sizeof nnz, cudaMemcpyDeviceToHost, s));
+  WM_CUDA(cudaStreamSynchronize(s));
+  int32_t *unbr = nullptr;
+  WM_CUDA(cudaMallocFromPoolAsync(reinterpret_cast<void **>(&unbr),
+                                  sizeof(int32_t) * (nnz > 0 ? nnz : 1), g->ws->pool, s));
+  union_rows_kernel<<<blocks, 256, 0, s>>>(ix->tasks, ix->dag_off, ix->bm_off,
+                                           g->ws->arena.as<uint32_t>(), nwide, nunion, dmoff,
+                                           nullptr, uoff, unbr);
+  WM_CUDA(cudaGetLastError());
+  cudaFreeAsync(dmoff, s);
+  cudaFreeAsync(udeg, s);
+  cudaFreeAsync(tmp, s);
+  Graph *ug = new Graph();
+  ug->n = U;
+  ug->nnz = nnz;
+  ug->device = g->device;
+  ug->num_sms = g->num_sms;
+  ug->ws = g->ws;
+  ug->offsets = uoff;
+  ug->neighbors = unbr;
+  ug->max_degree = sd[nwide];  // a component has at most d vertices
+  ix->ug = ug;
+  return WM_OK;
+}
+
 int run_clique(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_result *res, cudaStream_t s) {
   std::vector<std::vector<int32_t>> wide;
   int st = run_clique_impl(g, app, cfg, res, s, &wide, true);
@@ -1772,6 +1928,7 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   unsigned long long skip = 0, ntask = 0, arena_words = 0;
   const int64_t *doff_p = nullptr;
   const int32_t *dnbr_p = nullptr;
+  Graph *union_g = nullptr;  // set: the wide classes run as this graph's (k-1)-cliques
   int32_t *tasks_sorted = nullptr;
   const unsigned long long *bm_off = nullptr;
   if (ix) {
@@ -1809,6 +1966,23 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
     bm_off = ix->bm_off + skip;
     arena_words = ix->arena_words;
     res->launches = 1;
+    // the W = 8..32 classes run as the union graph's (k-1)-cliques instead
+    // (clique_union_get); not for the B_alg pass (its bytes are the parent's
+    // tree) or k = 3 (no level left to split).  WM_CLIQUE_UNION=0 disables.
+    const char *un = getenv("WM_CLIQUE_UNION");
+    if (!bytes && k >= 4 && !(un && *un == '0') && (hb[3] || hb[4] || hb[5])) {
+      if ((st = clique_union_get(g, ix, order, s))) return st;
+      if (ix->ug) {
+        union_g = ix->ug;
+        // the union roots are the sorted prefix with 128 < d <= 1024; with
+        // hb[3..5] cleared, tasks_sorted + (hb[5]+hb[4]+hb[3]) is the W <= 4 range
+        const unsigned long long shift = hb[5] + hb[4] + hb[3];
+        tasks_sorted += shift;
+        bm_off += shift;
+        ntask -= shift;
+        hb[3] = hb[4] = hb[5] = 0;
+      }
+    }
     pt.mark("plan");
   } else {
   if ((st = g->ws->dag_off.ensure(sizeof(int64_t) * (n + 1)))) return st;
@@ -2135,6 +2309,37 @@ static int run_clique_impl(Graph *g, const wm_app *app, const wm_cfg *cfg, wm_re
   res->idle_warp_fraction = tot_w > 0 ? idle_w / tot_w : 0;
   res->idle_warp_fraction_tail = tot_w > 0 ? idle_tail_w / tot_w : 0;
   res->peak_ext = (uint64_t)max_w * 32;
+  if (union_g) {
+    wm_app ua = *app;
+    ua.k = k - 1;
+    wm_cfg uc = *cfg;
+    uc.root_begin = uc.root_end = -1;
+    uc.order = WM_ORDER_DEGREE;
+    wm_result r = {};
+    std::vector<std::vector<int32_t>> nested;  // components have <= 1024 vertices: none
+    if ((st = run_clique_impl(union_g, &ua, &uc, &r, s, &nested, true))) return st;
+    res->clique_count += r.clique_count;
+    res->leaves += r.leaves;
+    res->nodes += r.nodes;
+    res->polls += r.polls;
+    res->tasks += r.tasks;
+    res->kernel_ms += r.kernel_ms;
+    res->device_ms += r.device_ms;
+    res->build_ms += r.build_ms;
+    res->launches += r.launches;
+    res->migrations += r.migrations;
+    res->rebalance_count += r.rebalance_count;
+    res->d2h_bytes += r.d2h_bytes;
+    if (r.warps > res->warps) res->warps = r.warps;
+    if (r.bucket_words > res->bucket_words) res->bucket_words = r.bucket_words;
+    // warp-time weighted idle fractions of the two launches' spans
+    const double a0 = res->kernel_ms - r.kernel_ms, a1 = r.kernel_ms;
+    if (a0 + a1 > 0) {
+      res->idle_warp_fraction = (res->idle_warp_fraction * a0 + r.idle_warp_fraction * a1) / (a0 + a1);
+      res->idle_warp_fraction_tail =
+          (res->idle_warp_fraction_tail * a0 + r.idle_warp_fraction_tail * a1) / (a0 + a1);
+    }
+  }
   return WM_OK;
 }
 
