@@ -605,6 +605,14 @@ def motif_block(args, stream, flush, gold, peak, peak_src, ncu):
         rb = run_motifs(g, k, d, mode="opt", balance_config=lb, roots=roots, stream=stream,
                         count_bytes=True)
         ach = rb.alg_bytes / (kms * 1e-3) / 1e9
+        mi = ncu.get("motif_enum_kernel", {}).get("%s_%s_issue" % (cfg, key))
+        if mi and clk:
+            pk = 4 * 148 * clk["sm_mhz"] * 1e6
+            ai = mi["warp_inst_per_launch"] / (kms * 1e-3)
+            rec["roofline_issue"] = {"bound": "issue", "achieved": ai, "peak": pk,
+                                     "unit": "warp-inst/s", "frac": ai / pk,
+                                     "ncu_issue_active": mi.get("issue_active"),
+                                     "source": mi.get("source")}
         rec["roofline"] = {"bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s",
                            "frac": ach / peak, "traffic": traffic,
                            "alg_bytes_per_launch": rb.alg_bytes, "peak_source": peak_src,
