@@ -204,12 +204,22 @@ def test_app_validation():
 def test_run_argument_errors_before_device():
     g = complete_graph(5)
     for kw in ({"mode": "bogus"}, {"warps": 0}, {"lane_width": 0},
-               {"mode": "wc", "balance_config": BalanceConfig()}, {"order": "random"}):
+               {"mode": "wc", "balance_config": BalanceConfig()}, {"order": "random"},
+               {"shard": (2, 2)}, {"shard": (0, 0)}, {"shard": (-1, 3)}):
         with pytest.raises(ValueError):
             run(g, clique_app(3), **kw)
     with pytest.raises(ValueError):
         run(g, Application(name="u", k=3, extend_all=False, genedges=False,
                            pipeline=(("filter", lambda *a: True, ()),), aggregator="counter"))
+
+
+def test_default_shard_is_local():
+    """A plain call never becomes a collective: without shard= the run is
+    (0, 1) even inside an initialised process group; "auto" asks the group."""
+    import inspect
+    from paper_2212_04551_b200 import engine, parallel
+    assert inspect.signature(engine.run).parameters["shard"].default is None
+    assert parallel.default_shard() == (0, 1)  # no process group here
 
 
 def test_balance_config():
