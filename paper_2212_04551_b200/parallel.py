@@ -138,8 +138,9 @@ def allreduce_device(res, vec, stream=None, group=None):
     u = v.view(np.uint64)
     P = len(res.pattern_counts) if res.pattern_counts is not None else 0
     base = _native.WM_RED_HIST + P
-    slots = v[base:base + _native.WM_RED_SLOT_WORDS * world].view(np.float64)
-    tmax = slots.reshape(world, _native.WM_RED_SLOT_WORDS).max(axis=0)
+    nslot = (v.size - base) // _native.WM_RED_SLOT_WORDS  # the shard count of the run
+    slots = v[base:base + _native.WM_RED_SLOT_WORDS * nslot].view(np.float64)
+    tmax = slots.reshape(nslot, _native.WM_RED_SLOT_WORDS).max(axis=0)
     return replace(res,
                    clique_count=int(u[_native.WM_RED_CLIQUES])
                    if res.clique_count is not None else None,
