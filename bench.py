@@ -484,7 +484,7 @@ def main():
     clique_ncu = ncu.get("clique_enum_kernel", {})
     issue = None
     ci = clique_ncu.get("issue_k%d" % args.k)
-    if ci and clk:
+    if ci and clk and world == 1:  # the ncu figure is a whole single-GPU launch
         # warp instructions per launch (ncu, same build) over the live kernel
         # time, against 4 issue slots per SM per cycle at the sampled clock
         peak_issue = 4 * 148 * clk["sm_mhz"] * 1e6
