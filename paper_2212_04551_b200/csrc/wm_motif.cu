@@ -128,8 +128,16 @@ struct MotifWarp {
   long long tb[kMaxK], te[kMaxK];   // CSR row bounds of tr[j]
   unsigned long long bm[kMaxK];     // bm[L-1] = bitmap of tr[0..L) (<= 54 bits, k <= 12)
   unsigned long long tail_cache;    // listing: last consumer tail seen (lane 0)
-  int32_t le[32];                   // listing: leaf vertex of record rank r
-  uint32_t lm[32];                  //          and its adjacency mask
+  union {
+    struct {
+      int32_t le[32];               // listing: leaf vertex of record rank r
+      uint32_t lm[32];              //          and its adjacency mask
+    };
+    struct {                        // counting: leaf_bulk's pair rings
+      uint2 ra[64];                 //   A leaves (x entry, e entry)
+      uint2 rb[64];                 //   B leaves (x entry, e vertex)
+    };
+  };
   uint32_t size[kMaxK], cur[kMaxK], lo[kMaxK];
   // B_alg: the node of length L is productive iff a leaf lies
   // below it.  claimed bit L: this warp knows the node's bytes are counted
@@ -583,6 +591,201 @@ __device__ __forceinline__ bool share_claims(const MotifArgs &a, MotifWarp &w, i
 #ifndef WM_MOTIF_MINBLOCKS_DEEP
 #define WM_MOTIF_MINBLOCKS_DEEP 6
 #endif
+#ifndef WM_MOTIF_LEAF_BULK
+#define WM_MOTIF_LEAF_BULK 1
+#endif
+
+// multi-GPU dealing (MotifArgs::l1_offset): true when the entry popped at
+// level s (vertex v, index cur - 1) belongs to another shard
+__device__ __forceinline__ bool other_shard(const MotifArgs &a, const MotifWarp &w, int s,
+                                            uint32_t cur, int32_t v) {
+  if (a.l1_stride <= 1) return false;
+  if (s == 1 && a.shard_level == 1)
+    return ((cur - 1) + (uint32_t)w.tr[0]) % a.l1_stride != a.l1_offset;
+  if (s == 2 && a.shard_level == 2) {
+    uint32_t h = (uint32_t)w.tr[0] * 0x9E3779B1u ^ (uint32_t)w.tr[1] * 0x85EBCA77u ^
+                 (uint32_t)v * 0xC2B2AE3Du;
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    return h % a.l1_stride != a.l1_offset;
+  }
+  return false;
+}
+
+// On-device load balancing, one poll (after each node): when enough warps are
+// idle, donate half of the pending entries of the shallowest level s0..s that
+// has >= 2 (reference balance.py:102-128 steals the shallowest pending entry).
+template <bool BYTES>
+__device__ __forceinline__ void poll_donate(const MotifArgs &a, MotifWarp &w, int s0, int s,
+                                            int &poll, unsigned long long &polls) {
+  const int lane = lane_id();
+  if (!(a.lb_on && ++poll >= a.lb_poll)) return;
+  poll = 0;
+  ++polls;
+  if (!donation_wanted(a.L, a.idle_min)) return;
+  int sd = -1;
+  for (int j = s0; j <= s; ++j)
+    if (w.cur[j] - w.lo[j] >= 2u) { sd = j; break; }
+  if (sd < 0) return;
+  const uint32_t pend = w.cur[sd] - w.lo[sd];
+  bool worth = sd < a.k - 2 || (unsigned long long)pend * w.size[sd] >= WM_MOTIF_DONATE_MIN;
+  if (BYTES && worth) {
+    int ok_share = 0;
+    if (lane == 0) ok_share = share_claims(a, w, sd);
+    worth = __shfl_sync(0xffffffffu, ok_share, 0) != 0;
+    __syncwarp();  // lane 0's claim slots visible to the record build
+  }
+  if (!worth) return;
+  const uint32_t half = pend / 2;
+  const uint32_t lo = w.lo[sd];
+  Rec3 r;
+#pragma unroll
+  for (int q = 0; q < 3; ++q) {
+    const int idx = 32 * q + lane;
+    uint32_t val = 0;
+    if (idx == 0) val = (uint32_t)w.tr[0];
+    else if (idx == 1) val = (uint32_t)sd;
+    else if (idx == 2) val = lo;
+    else if (idx == 3) val = lo + half;
+    else if (idx == 4) val = (uint32_t)w.bm[sd - 1];
+    else if (idx == 5) val = (uint32_t)(w.bm[sd - 1] >> 32);
+    else if (idx >= kMotifHdr && idx < kMotifHdr + sd - 1) val = (uint32_t)w.tr[idx - kMotifHdr + 1];
+    else if (BYTES && idx == kMotifClaimMask) val = w.claimed & ((2u << sd) - 1u);
+    else if (BYTES && idx >= kMotifClaim && idx < kMotifClaim + sd)
+      val = w.claim[idx - kMotifClaim + 1];
+    r.w[q] = val;
+  }
+  donate_record(a.L, r);
+  if (lane == 0) {
+    w.lo[sd] = lo + half;
+    atomicAdd(&a.L.lb->migrations, (unsigned long long)half);
+    atomicAdd(&a.L.lb->donation_polls, 1ull);
+  }
+  __syncwarp();
+}
+
+// One round of leaf_bulk's A ring: each lane takes one leaf (x, e) with e in
+// E_L, e > x — the A part of aggregate_leaves for its own x — probes
+// adj(e, x), looks the leaf's bitmap up and bumps the histogram.
+__device__ __forceinline__ uint32_t leaf_round_a(const MotifArgs &a, const uint2 *ring, int head,
+                                                 int cnt, uint32_t bml, int offL, int offK,
+                                                 int L, unsigned long long *sh, bool &bad) {
+  const int lane = lane_id();
+  bool valid = false;
+  uint32_t pid = 0;
+  if (lane < cnt) {
+    const uint2 p = ring[(head + lane) & 63];
+    const int32_t x = (int32_t)(p.x & a.vmask), e = (int32_t)(p.y & a.vmask);
+    const uint32_t adj = edge_hash_contains(a.H, e, x) ? 1u : 0u;
+    const uint32_t mask = (p.y >> a.vbits) | (adj << L);
+    pid = dict_lookup(a, bml | ((p.x >> a.vbits) << offL) | (mask << offK));
+    valid = true;
+    bad |= pid >= a.pattern_count;
+  }
+  hist_add(a, sh, valid && pid < a.pattern_count, pid);
+  return __popc(__ballot_sync(0xffffffffu, valid));
+}
+
+// One round of the B ring: lane takes one (x, e), e in N(x), e > tr[0]; e is
+// a leaf iff it is adjacent to none of tr[0..L) (its mask is 1 << L).
+__device__ __forceinline__ uint32_t leaf_round_b(const MotifArgs &a, const MotifWarp &w,
+                                                 const uint2 *ring, int head, int cnt,
+                                                 uint32_t bml, int offL, int offK, int L,
+                                                 unsigned long long *sh, bool &bad) {
+  const int lane = lane_id();
+  bool keep = false;
+  uint32_t pid = 0;
+  if (lane < cnt) {
+    const uint2 p = ring[(head + lane) & 63];
+    keep = adj_none(a, w, L, (int32_t)p.y);
+    if (keep) {
+      pid = dict_lookup(a, bml | ((p.x >> a.vbits) << offL) | ((1u << L) << offK));
+      bad |= pid >= a.pattern_count;
+    }
+  }
+  hist_add(a, sh, keep && pid < a.pattern_count, pid);
+  return __popc(__ballot_sync(0xffffffffu, keep));
+}
+
+// All pending children x of a node of length L = k-2 (entries [lo, cur) of
+// E_L), i.e. every leaf-parent below it, in one pass.  aggregate_leaves per x
+// leaves most lanes idle: E_L holds ~30-70 entries of which half exceed x, and
+// N(x) above tr[0] ~10 (cfg4/cfg5 counters, profiles/r02_motif_prof.log).
+// Here the leaves of successive x are flattened through two 64-entry rings
+// in shared memory — A leaves (x, e in E_L, e > x) and B leaves (x, e in
+// N(x), e > tr[0]) — and resolved 32 at a time, one leaf per lane: the
+// probes, dictionary lookups and histogram updates run with full lanes.
+// Same leaves, same patterns as the per-x pass (the histogram is a sum);
+// balancer polls and shard dealing stay per x.
+template <bool BYTES>
+__device__ __forceinline__ unsigned long long leaf_bulk(const MotifArgs &a, MotifWarp &w,
+                                                        uint32_t *base, unsigned long long *sh,
+                                                        int s0, int &poll,
+                                                        unsigned long long &polls,
+                                                        unsigned long long &nodes) {
+  const int lane = lane_id();
+  const uint32_t lt = (1u << lane) - 1u;
+  const int L = a.k - 2;
+  const uint32_t *src = level_ptr(a, base, L);
+  const uint32_t n = w.size[L];
+  const uint32_t bml = (uint32_t)w.bm[L - 1];  // bitmap of tr[0..L) (k <= 8)
+  const int offL = group_off(L), offK = group_off(L + 1);
+  const int32_t t0 = w.tr[0];
+  unsigned long long total = 0;
+  bool bad = false;
+  int ha = 0, na = 0, hb = 0, nb = 0;  // warp-uniform ring state
+  for (;;) {
+    const uint32_t cur = w.cur[L];
+    if (cur == w.lo[L]) break;
+    const uint32_t ex = __ldcg(src + (cur - 1));
+    const int32_t x = (int32_t)(ex & a.vmask);
+    __syncwarp();  // every lane's read of w.cur precedes lane 0's write
+    if (lane == 0) w.cur[L] = cur - 1;
+    __syncwarp();
+    if (other_shard(a, w, L, cur, x)) continue;
+    ++nodes;
+    // A leaves: e in E_L above x
+    for (uint32_t i0 = 0; i0 < n; i0 += 32) {
+      const uint32_t i = i0 + lane;
+      const uint32_t ent = i < n ? __ldcg(src + i) : 0u;
+      const bool keep = i < n && (int32_t)(ent & a.vmask) > x;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) w.ra[(ha + na + __popc(bal & lt)) & 63] = make_uint2(ex, ent);
+      na += __popc(bal);
+      if (na >= 32) {
+        __syncwarp();
+        total += leaf_round_a(a, w.ra, ha, 32, bml, offL, offK, L, sh, bad);
+        __syncwarp();
+        ha = (ha + 32) & 63;
+        na -= 32;
+      }
+    }
+    // B leaves: N(x) above tr[0] (rows ascending)
+    const long long xe = __ldg(a.off + x + 1);
+    for (long long p0 = row_first_above(a.nbr, __ldg(a.off + x), xe, t0); p0 < xe; p0 += 32) {
+      const long long p = p0 + lane;
+      const bool keep = p < xe;
+      const unsigned bal = __ballot_sync(0xffffffffu, keep);
+      if (keep) w.rb[(hb + nb + lane) & 63] = make_uint2(ex, (uint32_t)__ldg(a.nbr + p));
+      nb += __popc(bal);
+      if (nb >= 32) {
+        __syncwarp();
+        total += leaf_round_b(a, w, w.rb, hb, 32, bml, offL, offK, L, sh, bad);
+        __syncwarp();
+        hb = (hb + 32) & 63;
+        nb -= 32;
+      }
+    }
+    poll_donate<BYTES>(a, w, s0, L, poll, polls);
+  }
+  __syncwarp();
+  if (na) total += leaf_round_a(a, w.ra, ha, na, bml, offL, offK, L, sh, bad);
+  if (nb) total += leaf_round_b(a, w, w.rb, hb, nb, bml, offL, offK, L, sh, bad);
+  __syncwarp();
+  if (__any_sync(0xffffffffu, bad) && lane == 0) raise_error(a.L.lb, WM_EINVARIANT);
+  return total;
+}
 
 template <bool BYTES, bool LIST, int MINB>
 __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
@@ -681,27 +884,23 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
         --s;
         continue;
       }
-      if (s == 1 && a.shard_level == 1 && a.l1_stride > 1 &&
-          ((cur - 1) + (uint32_t)w.tr[0]) % a.l1_stride != a.l1_offset) {
-        // another shard's edge task: consume without descending
-        if (lane == 0) w.cur[1] = cur - 1;
-        __syncwarp();
+#if WM_MOTIF_LEAF_BULK
+      if (!BYTES && !LIST && s == k - 2 && k >= 4 && a.H.b) {
+        // the node's children are leaf-parents: all of them in one pass
+        WM_PT(tl);
+        leaves += leaf_bulk<BYTES>(a, w, base, sh, s0, poll, polls, nodes);
+        WM_PACC(3, tl);
         continue;
       }
+#endif
       // move_step: pop the highest pending entry (engine.py:652-669)
       const uint32_t ent = __ldcg(level_ptr(a, base, s) + (cur - 1));
       const int32_t v = (int32_t)(ent & a.vmask);
-      if (s == 2 && a.shard_level == 2 && a.l1_stride > 1) {
-        uint32_t h = (uint32_t)w.tr[0] * 0x9E3779B1u ^ (uint32_t)w.tr[1] * 0x85EBCA77u ^
-                     (uint32_t)v * 0xC2B2AE3Du;
-        h ^= h >> 15;
-        h *= 0x2C1B3C6Du;
-        h ^= h >> 12;
-        if (h % a.l1_stride != a.l1_offset) {  // another shard's (root, child, grandchild)
-          if (lane == 0) w.cur[2] = cur - 1;
-          __syncwarp();
-          continue;
-        }
+      if (other_shard(a, w, s, cur, v)) {
+        // another shard's edge task / (root, child, grandchild): consume without descending
+        if (lane == 0) w.cur[s] = cur - 1;
+        __syncwarp();
+        continue;
       }
       const uint32_t m = ent >> a.vbits;
       set_tr(a, w, s, v);
@@ -755,54 +954,7 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
         ++s;
       }
       // on-device load balancing: donate half of the shallowest pending range
-      if (a.lb_on && ++poll >= a.lb_poll) {
-        poll = 0;
-        ++polls;
-        if (donation_wanted(a.L, a.idle_min)) {
-          int sd = -1;
-          for (int j = s0; j <= s; ++j)
-            if (w.cur[j] - w.lo[j] >= 2u) { sd = j; break; }
-          if (sd >= 0) {
-            const uint32_t pend = w.cur[sd] - w.lo[sd];
-            bool worth =
-                sd < k - 2 || (unsigned long long)pend * w.size[sd] >= WM_MOTIF_DONATE_MIN;
-            if (BYTES && worth) {
-              int ok_share = 0;
-              if (lane == 0) ok_share = share_claims(a, w, sd);
-              worth = __shfl_sync(0xffffffffu, ok_share, 0) != 0;
-              __syncwarp();  // lane 0's claim slots visible to the record build
-            }
-            if (worth) {
-              const uint32_t half = pend / 2;
-              const uint32_t lo = w.lo[sd];
-              Rec3 r;
-#pragma unroll
-              for (int q = 0; q < 3; ++q) {
-                const int idx = 32 * q + lane;
-                uint32_t val = 0;
-                if (idx == 0) val = (uint32_t)w.tr[0];
-                else if (idx == 1) val = (uint32_t)sd;
-                else if (idx == 2) val = lo;
-                else if (idx == 3) val = lo + half;
-                else if (idx == 4) val = (uint32_t)w.bm[sd - 1];
-                else if (idx == 5) val = (uint32_t)(w.bm[sd - 1] >> 32);
-                else if (idx >= kMotifHdr && idx < kMotifHdr + sd - 1) val = (uint32_t)w.tr[idx - kMotifHdr + 1];
-                else if (BYTES && idx == kMotifClaimMask) val = w.claimed & ((2u << sd) - 1u);
-                else if (BYTES && idx >= kMotifClaim && idx < kMotifClaim + sd)
-                  val = w.claim[idx - kMotifClaim + 1];
-                r.w[q] = val;
-              }
-              donate_record(a.L, r);
-              if (lane == 0) {
-                w.lo[sd] = lo + half;
-                atomicAdd(&a.L.lb->migrations, (unsigned long long)half);
-                atomicAdd(&a.L.lb->donation_polls, 1ull);
-              }
-              __syncwarp();
-            }
-          }
-        }
-      }
+      poll_donate<BYTES>(a, w, s0, s, poll, polls);
     }
   }
   leaves = __shfl_sync(0xffffffffu, leaves, 0);
