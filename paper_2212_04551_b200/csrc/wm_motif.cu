@@ -595,6 +595,7 @@ __device__ __forceinline__ bool share_claims(const MotifArgs &a, MotifWarp &w, i
 #define WM_MOTIF_LEAF_BULK 1
 #endif
 
+
 // multi-GPU dealing (MotifArgs::l1_offset): true when the entry popped at
 // level s (vertex v, index cur - 1) belongs to another shard
 __device__ __forceinline__ bool other_shard(const MotifArgs &a, const MotifWarp &w, int s,
@@ -616,14 +617,25 @@ __device__ __forceinline__ bool other_shard(const MotifArgs &a, const MotifWarp 
 // On-device load balancing, one poll (after each node): when enough warps are
 // idle, donate half of the pending entries of the shallowest level s0..s that
 // has >= 2 (reference balance.py:102-128 steals the shallowest pending entry).
+// The poll is software-pipelined: the idle/donor ticket counters loaded at
+// one poll (lane 0, into lbt/lbh) are consumed at the next, so the L2 round
+// trip never stalls the enumeration (cfg4 k=6 87.9 -> 84.9 ms, idle fraction
+// 0.098 -> 0.026; cfg5 k=7 28.3 -> 26.2, profiles/r02_ab_motif_v2.log).
 template <bool BYTES>
 __device__ __forceinline__ void poll_donate(const MotifArgs &a, MotifWarp &w, int s0, int s,
-                                            int &poll, unsigned long long &polls) {
+                                            int &poll, unsigned long long &polls, uint32_t &lbt,
+                                            uint32_t &lbh) {
   const int lane = lane_id();
   if (!(a.lb_on && ++poll >= a.lb_poll)) return;
   poll = 0;
   ++polls;
-  if (!donation_wanted(a.L, a.idle_min)) return;
+  int want = 0;
+  if (lane == 0) {
+    want = (int)(lbt - lbh) >= a.idle_min;
+    lbt = (uint32_t)ld_relaxed(&a.L.lb->tail);
+    lbh = (uint32_t)ld_relaxed(&a.L.lb->head);
+  }
+  if (!__shfl_sync(0xffffffffu, want, 0)) return;
   int sd = -1;
   for (int j = s0; j <= s; ++j)
     if (w.cur[j] - w.lo[j] >= 2u) { sd = j; break; }
@@ -723,7 +735,8 @@ __device__ __forceinline__ unsigned long long leaf_bulk(const MotifArgs &a, Moti
                                                         uint32_t *base, unsigned long long *sh,
                                                         int s0, int &poll,
                                                         unsigned long long &polls,
-                                                        unsigned long long &nodes) {
+                                                        unsigned long long &nodes,
+                                                        uint32_t &lbt, uint32_t &lbh) {
   const int lane = lane_id();
   const uint32_t lt = (1u << lane) - 1u;
   const int L = a.k - 2;
@@ -761,9 +774,10 @@ __device__ __forceinline__ unsigned long long leaf_bulk(const MotifArgs &a, Moti
         na -= 32;
       }
     }
-    // B leaves: N(x) above tr[0] (rows ascending)
-    const long long xe = __ldg(a.off + x + 1);
-    for (long long p0 = row_first_above(a.nbr, __ldg(a.off + x), xe, t0); p0 < xe; p0 += 32) {
+    // B leaves: N(x) above tr[0] (rows ascending; a scan from the row start
+    // with an e > tr[0] test measured the same, profiles/r02_ab_motif_v2.log)
+    const long long xb = __ldg(a.off + x), xe = __ldg(a.off + x + 1);
+    for (long long p0 = row_first_above(a.nbr, xb, xe, t0); p0 < xe; p0 += 32) {
       const long long p = p0 + lane;
       const bool keep = p < xe;
       const unsigned bal = __ballot_sync(0xffffffffu, keep);
@@ -777,7 +791,7 @@ __device__ __forceinline__ unsigned long long leaf_bulk(const MotifArgs &a, Moti
         nb -= 32;
       }
     }
-    poll_donate<BYTES>(a, w, s0, L, poll, polls);
+    poll_donate<BYTES>(a, w, s0, L, poll, polls, lbt, lbh);
   }
   __syncwarp();
   if (na) total += leaf_round_a(a, w.ra, ha, na, bml, offL, offK, L, sh, bad);
@@ -810,6 +824,7 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
   bool ok = true;
   if (LIST && lane == 0) w.tail_cache = 0;
   int poll = 0;
+  uint32_t lbt = 0, lbh = 0;  // poll_donate's pipelined ticket counters (lane 0)
 #if WM_MOTIF_PROF
   unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -888,7 +903,7 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
       if (!BYTES && !LIST && s == k - 2 && k >= 4 && a.H.b) {
         // the node's children are leaf-parents: all of them in one pass
         WM_PT(tl);
-        leaves += leaf_bulk<BYTES>(a, w, base, sh, s0, poll, polls, nodes);
+        leaves += leaf_bulk<BYTES>(a, w, base, sh, s0, poll, polls, nodes, lbt, lbh);
         WM_PACC(3, tl);
         continue;
       }
@@ -954,7 +969,7 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
         ++s;
       }
       // on-device load balancing: donate half of the shallowest pending range
-      poll_donate<BYTES>(a, w, s0, s, poll, polls);
+      poll_donate<BYTES>(a, w, s0, s, poll, polls, lbt, lbh);
     }
   }
   leaves = __shfl_sync(0xffffffffu, leaves, 0);
