@@ -571,9 +571,11 @@ def motif_block(args, stream, flush, gold, peak, peak_src, ncu):
     through ``run_motifs`` from pinned host buffers and the CPU reference on a
     fixed root subset."""
     from paper_2212_04551_b200 import BalanceConfig, build_dictionary, run_motifs, synth
-    lb = BalanceConfig(threshold=1.0, poll_interval=2)
     out = {}
     for cfg, k, suffix, off_suffix in MOTIF_WORKLOADS:
+        # balancer poll every 4 DFS steps at k <= 5, every 8 deeper (leaf_bulk
+        # polls per leaf-parent; profiles/r02_ab_motif_poll.log)
+        lb = BalanceConfig(threshold=1.0, poll_interval=4 if k <= 5 else 8)
         g = synth.config_graph(cfg)
         d = build_dictionary(k)
         key = "k%d_s%d" % (k, suffix)
