@@ -577,8 +577,10 @@ __device__ __forceinline__ bool share_claims(const MotifArgs &a, MotifWarp &w, i
 }
 
 // a leaf-level range is donated only if it carries >= this many candidate scans
+// (4,096 after leaf_bulk: cfg5 k=7 26.7 -> 26.0 ms, cfg4 k=6 83.9 -> 83.5, k=5
+// unchanged; 16,384 and 256 slower, profiles/r02_ab_motif_donate.log)
 #ifndef WM_MOTIF_DONATE_MIN
-#define WM_MOTIF_DONATE_MIN 1024ull
+#define WM_MOTIF_DONATE_MIN 4096ull
 #endif
 // blocks per SM the register budget must allow: 4 (64 registers) for k <= 5,
 // 6 (40 registers) for k >= 6, where the longer subtrees hide the spill cost
