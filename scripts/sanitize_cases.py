@@ -39,11 +39,16 @@ for gname, g in graphs.items():
                   run_clique(g, k, mode=mode, **kw).clique_count, want)
         check("clique %s k=%d id-order" % (gname, k),
               run_clique(g, k, mode="opt", balance_config=LB, order="id").clique_count, want)
-    for k in (3, 4, 5):
+    for k in (3, 4, 5, 6):
         d = build_dictionary(k)
         want = oracle.motif_run(g, k, d.table, d.pattern_count, threads=2)
         r = run_motifs(g, k, d, mode="opt", balance_config=LB)
         check("motif %s k=%d opt" % (gname, k), r.pattern_counts, want["hist"])
+        # two shards (level-1 / level-2 dealing inside leaf_bulk): their sum
+        parts = [run_motifs(g, k, d, mode="opt", balance_config=LB, shard=(r_, 2),
+                            reduce=False).pattern_counts for r_ in range(2)]
+        check("motif %s k=%d 2 shards" % (gname, k), [a + b for a, b in zip(*parts)],
+              want["hist"])
         r = run_motifs(g, k, d, mode="opt", balance_config=LB, count_bytes=True)
         check("motif %s k=%d B_alg" % (gname, k), r.alg_bytes, want["alg_bytes"])
     for k in (3, 4):
