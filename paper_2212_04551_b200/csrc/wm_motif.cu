@@ -145,6 +145,10 @@ struct MotifWarp {
   // with other warps through a donation (kNoClaim: private to this warp).
   uint32_t claim[kMaxK];
   uint32_t claimed;
+  // per-warp counters (lane 0), in shared memory rather than registers: the
+  // k >= 6 kernel runs at 40 registers (6 blocks/SM) and spills
+  unsigned long long n_leaves, n_nodes, n_polls, n_peak, n_tasks;
+  uint32_t lbt, lbh;  // poll_donate's pipelined ticket counters (lane 0)
 };
 
 constexpr uint32_t kNoClaim = 0xFFFFFFFFu;
@@ -625,17 +629,16 @@ __device__ __forceinline__ bool other_shard(const MotifArgs &a, const MotifWarp 
 // 0.098 -> 0.026; cfg5 k=7 28.3 -> 26.2, profiles/r02_ab_motif_v2.log).
 template <bool BYTES>
 __device__ __forceinline__ void poll_donate(const MotifArgs &a, MotifWarp &w, int s0, int s,
-                                            int &poll, unsigned long long &polls, uint32_t &lbt,
-                                            uint32_t &lbh) {
+                                            int &poll) {
   const int lane = lane_id();
   if (!(a.lb_on && ++poll >= a.lb_poll)) return;
   poll = 0;
-  ++polls;
   int want = 0;
   if (lane == 0) {
-    want = (int)(lbt - lbh) >= a.idle_min;
-    lbt = (uint32_t)ld_relaxed(&a.L.lb->tail);
-    lbh = (uint32_t)ld_relaxed(&a.L.lb->head);
+    ++w.n_polls;
+    want = (int)(w.lbt - w.lbh) >= a.idle_min;
+    w.lbt = (uint32_t)ld_relaxed(&a.L.lb->tail);
+    w.lbh = (uint32_t)ld_relaxed(&a.L.lb->head);
   }
   if (!__shfl_sync(0xffffffffu, want, 0)) return;
   int sd = -1;
@@ -735,10 +738,7 @@ __device__ __forceinline__ uint32_t leaf_round_b(const MotifArgs &a, const Motif
 template <bool BYTES>
 __device__ __forceinline__ unsigned long long leaf_bulk(const MotifArgs &a, MotifWarp &w,
                                                         uint32_t *base, unsigned long long *sh,
-                                                        int s0, int &poll,
-                                                        unsigned long long &polls,
-                                                        unsigned long long &nodes,
-                                                        uint32_t &lbt, uint32_t &lbh) {
+                                                        int s0, int &poll) {
   const int lane = lane_id();
   const uint32_t lt = (1u << lane) - 1u;
   const int L = a.k - 2;
@@ -759,7 +759,7 @@ __device__ __forceinline__ unsigned long long leaf_bulk(const MotifArgs &a, Moti
     if (lane == 0) w.cur[L] = cur - 1;
     __syncwarp();
     if (other_shard(a, w, L, cur, x)) continue;
-    ++nodes;
+    if (lane == 0) ++w.n_nodes;
     // A leaves: e in E_L above x
     for (uint32_t i0 = 0; i0 < n; i0 += 32) {
       const uint32_t i = i0 + lane;
@@ -793,7 +793,7 @@ __device__ __forceinline__ unsigned long long leaf_bulk(const MotifArgs &a, Moti
         nb -= 32;
       }
     }
-    poll_donate<BYTES>(a, w, s0, L, poll, polls, lbt, lbh);
+    poll_donate<BYTES>(a, w, s0, L, poll);
   }
   __syncwarp();
   if (na) total += leaf_round_a(a, w.ra, ha, na, bml, offL, offK, L, sh, bad);
@@ -821,12 +821,16 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
   WarpClock clk;
   warp_clock_begin(clk, a.L.lb);
   bool roots_left = true;
-  unsigned long long leaves = 0, bytes = 0, tasks_done = 0, nodes = 0, polls = 0, peak = 0;
+  unsigned long long bytes = 0;
   unsigned long long emitted = 0;
   bool ok = true;
   if (LIST && lane == 0) w.tail_cache = 0;
   int poll = 0;
-  uint32_t lbt = 0, lbh = 0;  // poll_donate's pipelined ticket counters (lane 0)
+  if (lane == 0) {
+    w.n_leaves = w.n_nodes = w.n_polls = w.n_peak = w.n_tasks = 0;
+    w.lbt = w.lbh = 0;
+  }
+  __syncwarp();
 #if WM_MOTIF_PROF
   unsigned long long prof[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #endif
@@ -854,7 +858,7 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
         w.lo[1] = 0;
       }
       s0 = 1;
-      ++tasks_done;
+      if (lane == 0) ++w.n_tasks;
     } else {
       // donated prefix: rebuild E_1..E_s0 deterministically, then own [lo, hi)
       s0 = (int)rec_word(rec, 1);
@@ -905,7 +909,8 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
       if (!BYTES && !LIST && s == k - 2 && k >= 4 && a.H.b) {
         // the node's children are leaf-parents: all of them in one pass
         WM_PT(tl);
-        leaves += leaf_bulk<BYTES>(a, w, base, sh, s0, poll, polls, nodes, lbt, lbh);
+        const unsigned long long got = leaf_bulk<BYTES>(a, w, base, sh, s0, poll);
+        if (lane == 0) w.n_leaves += got;
         WM_PACC(3, tl);
         continue;
       }
@@ -932,7 +937,7 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
                            : (w.bm[s - 1] | ((unsigned long long)m << group_off(s)));
       }
       __syncwarp();
-      ++nodes;
+      if (lane == 0) ++w.n_nodes;
       if (s + 1 == k - 1) {
         unsigned long long got;
         WM_PT(tl);
@@ -950,7 +955,7 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
           if (d > prof[5]) prof[5] = d;
         }
 #endif
-        leaves += got;
+        if (lane == 0) w.n_leaves += got;
         if (BYTES && lane == 0 && got) claim_path(a, w, s + 1, bytes);
         __syncwarp();
       } else {
@@ -964,24 +969,26 @@ __global__ void __launch_bounds__(256, MINB) motif_enum_kernel(MotifArgs a) {
           w.cur[s + 1] = n;
           w.lo[s + 1] = 0;
         }
+        if (lane == 0) {
+          unsigned long long live = 0;
+          for (int j = 1; j <= s + 1; ++j) live += w.size[j];
+          if (live > w.n_peak) w.n_peak = live;
+        }
         __syncwarp();
-        unsigned long long live = 0;
-        for (int j = 1; j <= s + 1; ++j) live += w.size[j];
-        if (live > peak) peak = live;
         ++s;
       }
       // on-device load balancing: donate half of the shallowest pending range
-      poll_donate<BYTES>(a, w, s0, s, poll, polls, lbt, lbh);
+      poll_donate<BYTES>(a, w, s0, s, poll);
     }
   }
-  leaves = __shfl_sync(0xffffffffu, leaves, 0);
+  __syncwarp();
   if (lane == 0) {
-    atomicAdd(&a.counters[0], leaves);
+    atomicAdd(&a.counters[0], w.n_leaves);
     if (BYTES) atomicAdd(&a.counters[1], bytes);
-    atomicAdd(&a.counters[2], tasks_done);
-    atomicAdd(&a.counters[3], nodes);
-    atomicAdd(&a.counters[4], polls);
-    atomicMax(&a.counters[5], peak);
+    atomicAdd(&a.counters[2], w.n_tasks);
+    atomicAdd(&a.counters[3], w.n_nodes);
+    atomicAdd(&a.counters[4], w.n_polls);
+    atomicMax(&a.counters[5], w.n_peak);
     if (LIST) atomicAdd(&a.counters[6], emitted);
 #if WM_MOTIF_PROF
     for (int q = 0; q < 7; ++q) {
