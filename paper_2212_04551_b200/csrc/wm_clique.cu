@@ -386,6 +386,10 @@ template <int WMAX> struct alignas(16) CliqueSmem {  // 16B: uint4 row loads
   uint32_t queue[96];                  // bulk4/5 ring (64) + a scratch slot per lane
   uint32_t pq[64];                     // bulk5 (h, i) pair ring
   uint32_t crow[32];                   // bulk4 node compacted to <= 32 members
+  // per-warp node/poll counters (lane 0): off the register budget, cfg3 k=9
+  // 18.95 -> 18.59 ms, k=10 81.7 -> 80.0 (profiles/r02_ab_clique_smem_counters.log;
+  // the poll's ticket words there too were slower)
+  unsigned long long n_nodes, n_polls;
 };
 
 struct CliqueArgs {
@@ -721,7 +725,7 @@ __device__ __forceinline__ unsigned long long bulk4_compact(CliqueSmem<WMAX> &sm
     }
     if (pollable && ++tc.poll >= a.lb_poll) {
       tc.poll = 0;
-      ++tc.polls;
+      if (lane == 0) ++sm.n_polls;
       int want = 0;
       if (lane == 0) {
         want = (int)(pt - ph) >= a.idle_min;
@@ -799,7 +803,7 @@ __device__ __forceinline__ unsigned long long bulk4(CliqueSmem<WMAX> &sm, const 
       }
       if (a.lb_on && ++tc.poll >= a.lb_poll) {
         tc.poll = 0;
-        ++tc.polls;
+        if (lane == 0) ++sm.n_polls;
         int want = 0;
         if (lane == 0) {
           want = (int)(pt - ph) >= a.idle_min;
@@ -924,7 +928,7 @@ __device__ __forceinline__ bool bulk5(CliqueSmem<WMAX> &sm, const CliqueArgs &a,
       // children (the pipelined loads keep it cheap; every child over-donates)
       if (pollable && ++tc.poll >= WM_BULK5_POLL_EVERY) {
         tc.poll = 0;
-        ++tc.polls;
+        if (lane == 0) ++sm.n_polls;
         int want = 0;
         if (lane == 0) {
           want = (int)(pt - ph) >= a.idle_min;
@@ -1130,7 +1134,7 @@ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
     }
     const int cnt = __reduce_add_sync(0xffffffffu, __popc(cw));
     __syncwarp();
-    ++tc.nodes;
+    if (lane == 0) ++sm.n_nodes;
     unsigned long long part5 = 0;
     bool done5 = false;
     if (!BYTES && k >= WM_BULK5_MINK && s + 1 == k - 5 && cnt >= k - s - 1) {
@@ -1173,7 +1177,7 @@ void run_task(CliqueSmem<WMAX> &sm, const CliqueArgs &a, int kind,
     // on-device load balancing (opt mode): poll the idle-warp ring
     if (!BYTES && a.lb_on && ++tc.poll >= a.lb_poll) {
       tc.poll = 0;
-      ++tc.polls;
+      if (lane == 0) ++sm.n_polls;
       int want = 0;
       if (lane == 0) {
         want = (int)(pt - ph) >= a.idle_min;
@@ -1205,6 +1209,8 @@ __global__ void __launch_bounds__(256, WMAX <= 4 ? WM_ENUM_MINBLOCKS
   warp_clock_begin(clk, a.L.lb);
   bool roots_left = true;
   TaskCounters tc = {0, 0, 0, 0, 0};
+  if (lane == 0) sm.n_nodes = sm.n_polls = 0;
+  __syncwarp();
   unsigned long long tasks_done = 0;
   unsigned long long cached = ~0ull;
   for (;;) {
@@ -1249,8 +1255,8 @@ __global__ void __launch_bounds__(256, WMAX <= 4 ? WM_ENUM_MINBLOCKS
     atomicAdd(&a.counters[0], acc);
     if (BYTES) atomicAdd(&a.counters[1], bytes);
     atomicAdd(&a.counters[2], tasks_done);
-    atomicAdd(&a.counters[3], tc.nodes);
-    atomicAdd(&a.counters[4], tc.polls);
+    atomicAdd(&a.counters[3], sm.n_nodes);
+    atomicAdd(&a.counters[4], sm.n_polls);
   }
   warp_clock_end(a.L.lb, clk);
 }
