@@ -586,16 +586,16 @@ __device__ __forceinline__ bool share_claims(const MotifArgs &a, MotifWarp &w, i
 #ifndef WM_MOTIF_DONATE_MIN
 #define WM_MOTIF_DONATE_MIN 4096ull
 #endif
-// blocks per SM the register budget must allow: 4 (64 registers) for k <= 5,
-// 6 (40 registers) for k >= 6, where the longer subtrees hide the spill cost
-// and the extra warps overlap the (L2-resident, suffix-local) hash probes:
-// cfg4 k=6 135.9 -> 128.4 ms, cfg5 k=7 43.8 -> 41.1; k=5 prefers 4 (3.68 vs
-// 3.78 ms) (profiles/r02_ab_motif_mb.log)
+// blocks per SM the register budget must allow.  Before leaf_bulk: 4 (64
+// registers) for k <= 5, 6 (40 registers) for k >= 6 (profiles/r02_ab_motif_mb.log).
+// With leaf_bulk and the per-warp counters in shared memory, 5 (48 registers)
+// for every k: cfg4 k=5 2.83 -> 2.69 ms, k=6 83.0 -> 79.9, cfg5 k=7 25.5 -> 25.2
+// (profiles/r02_ab_motif_occupancy_v2.log)
 #ifndef WM_MOTIF_MINBLOCKS
-#define WM_MOTIF_MINBLOCKS 4
+#define WM_MOTIF_MINBLOCKS 5
 #endif
 #ifndef WM_MOTIF_MINBLOCKS_DEEP
-#define WM_MOTIF_MINBLOCKS_DEEP 6
+#define WM_MOTIF_MINBLOCKS_DEEP 5
 #endif
 #ifndef WM_MOTIF_LEAF_BULK
 #define WM_MOTIF_LEAF_BULK 1
