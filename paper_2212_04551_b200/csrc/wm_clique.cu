@@ -551,7 +551,7 @@ __device__ __forceinline__ unsigned long long bulk3(const uint32_t *adj, const u
 #define WM_BULK5_POLL_MIN 4
 #endif
 #ifndef WM_BULK5_POLL_EVERY
-#define WM_BULK5_POLL_EVERY 4
+#define WM_BULK5_POLL_EVERY 8  // with donate min 32K: k=8 4.63 -> 4.37 ms, k=9 18.53 -> 18.24 (r02_ab_clique_knobs.log)
 #endif
 #ifndef WM_COMPACT_POLL_MIN
 #define WM_COMPACT_POLL_MIN 16
@@ -604,10 +604,11 @@ __device__ __forceinline__ unsigned long long bulk4_round(const uint32_t *adj, c
 // has any (reference balance.py:102-128 steals the shallowest pending entry;
 // one record here carries half of that level so a thief gets a large
 // subtree).  Record: [task, level, C[level] (w words), donated P (w words)].
-// Subtrees estimated below ~16K nodes are not worth a move and stay.
+// Subtrees estimated below ~32K nodes are not worth a move and stay (16K before the
+// per-warp counters and bulk5 poll every 8 children, profiles/r02_ab_clique_knobs.log).
 constexpr int kRecHdr = 2;
 #ifndef WM_CLIQUE_DONATE_MIN
-#define WM_CLIQUE_DONATE_MIN 16384.f
+#define WM_CLIQUE_DONATE_MIN 32768.f
 #endif
 
 template <int w>
